@@ -1,0 +1,223 @@
+/*
+ * gts.h -- C ABI of the B200-native GPUTreeShap hot path (arXiv 2010.13972).
+ *
+ * The four calls named by the method's four steps (§3):
+ *
+ *   (1) gts_extract_paths      extract one unique path per leaf and merge
+ *                              repeated features      (§3.1-3.2)
+ *   (2) gts_binpack            pack paths into 32-lane warps, FFD / BFD / NF /
+ *                              none, with utilisation (§3.3)
+ *   (3) gts_shap               SHAP values phi and bias phi_0 for every row
+ *                              (Eq. 1-2, Algorithm 1-3)
+ *   (4) gts_shap_interactions  SHAP interaction values (Eq. 3-6, §3.5;
+ *                              PAPER.md:120-139, 377-381)
+ *
+ * plus the device-layout step between (2) and (3): gts_blob_plan /
+ * gts_blob_write serialise the packed tables into one contiguous byte blob that
+ * the caller copies to device memory it owns (and, multi-GPU, broadcasts).
+ *
+ * Conventions (all functions):
+ *   - Every call returns gts_status; GTS_OK == 0.  On error a message is
+ *     available from gts_last_error() (thread-local, valid until the next call
+ *     on the same thread).  Argument errors are detected before any launch.
+ *   - Ownership: the caller owns every array it passes (model arrays: host;
+ *     X, blob, phi: device).  gts_paths and gts_bins are library-owned and must
+ *     be released with their _free functions.  The library keeps no global
+ *     state besides the thread-local error string.
+ *   - Device calls are asynchronous on the caller's stream (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream) and write only the given
+ *     output buffer.  Kernel launch failures map to GTS_ERR_CUDA.
+ *   - Thread safety: calls with distinct output buffers may run concurrently
+ *     from several host threads, streams or devices.
+ *   - Determinism: path tables, packings and blobs are bit-exact and
+ *     reproducible.  fp32/fp64 phi are accumulated with atomics across thread
+ *     blocks, so they are reproducible up to summation order.
+ */
+#ifndef GTS_H_
+#define GTS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GTS_ABI_VERSION 1
+#define GTS_WARP_CAPACITY 32 /* lanes per warp = bin capacity B */
+
+typedef enum gts_status {
+  GTS_OK = 0,
+  GTS_ERR_INVALID_ARGUMENT = 1, /* null pointer, negative size, bad enum, buffer too small */
+  GTS_ERR_INVALID_MODEL = 2,    /* cycle / dangling or shared child, feature out of range,
+                                   cover <= 0, cover(parent) != cover(l)+cover(r) beyond 1e-6
+                                   relative, non-finite threshold / value, bad group */
+  GTS_ERR_PATH_TOO_LONG = 3,    /* merged path length (root included) > 32 */
+  GTS_ERR_NONFINITE = 4,        /* reserved: non-finite X when validation is requested */
+  GTS_ERR_CUDA = 5,             /* CUDA launch / runtime error */
+  GTS_ERR_OUT_OF_MEMORY = 6     /* host allocation failed */
+} gts_status;
+
+/* Bin-packing heuristics (Table 1). */
+typedef enum gts_pack_algo {
+  GTS_PACK_FFD = 0,  /* first-fit decreasing */
+  GTS_PACK_BFD = 1,  /* best-fit decreasing (the paper's recommendation) */
+  GTS_PACK_NF = 2,   /* next-fit, arrival order */
+  GTS_PACK_NONE = 3  /* one path per warp (the Table 5 "none" baseline) */
+} gts_pack_algo;
+
+/* Arithmetic type of X, phi and the kernels. */
+typedef enum gts_dtype { GTS_F32 = 0, GTS_F64 = 1 } gts_dtype;
+
+/* Device layout of the blob = which kernel family runs it. */
+typedef enum gts_layout {
+  /* Row-lane kernels (default, B200-native): lanes = rows, one warp walks a
+     chunk of paths; the permutation-weight polynomial of each (row, path) is
+     EXTENDed / UNWOUND in the nodal basis. */
+  GTS_LAYOUT_NODAL = 0,
+  /* Paper-lineage kernels: lanes = path elements of the packed bins, EXTEND
+     via __shfl_up_sync and UNWOUNDSUM via __shfl_sync (Algorithms 2-3,
+     readings G4/G5), swap-to-end conditioning for interactions (§3.5). */
+  GTS_LAYOUT_WARP_BINS = 1
+} gts_layout;
+
+/*
+ * Tree ensemble: the node lists {v, a, b, t, r, d} of PAPER.md:114 in CSR over
+ * trees.  Caller-owned HOST arrays, read only during gts_extract_paths.
+ */
+typedef struct gts_model {
+  int64_t n_trees;              /* T >= 0 */
+  const int64_t* node_offset;   /* [T+1]; tree t owns nodes [node_offset[t], node_offset[t+1]);
+                                   node_offset[0] == 0; each tree >= 1 node; local node 0 = root */
+  const int32_t* left;          /* a_j: local index of the left child, -1 at leaves */
+  const int32_t* right;         /* b_j: local index of the right child, -1 at leaves */
+  const int32_t* feature;       /* d_j in [0, n_features) at internal nodes (ignored at leaves) */
+  const float* threshold;       /* t_j: split rule x[d_j] < t_j -> left (reading G1) */
+  const double* cover;          /* r_j > 0, training weight through node j */
+  const double* leaf_value;     /* v_j at leaves (ignored at internal nodes) */
+  const int32_t* tree_group;    /* [T] output group of each tree, in [0, n_groups) */
+  int32_t n_features;           /* M >= 1 */
+  int32_t n_groups;             /* G >= 1 (classes for multiclass, 1 for regression) */
+  double base_score;            /* added to the bias phi_0 of every group */
+} gts_model;
+
+/* ---------------------------------------------------------------- (1) paths */
+
+typedef struct gts_paths gts_paths; /* opaque, library-owned */
+
+/* Read-only view of the canonical path-element table (Listing 1).
+   Pointers stay valid until gts_paths_free. */
+typedef struct gts_paths_view {
+  int64_t n_paths;              /* L = number of leaves */
+  int64_t n_elems;              /* E = sum of merged path lengths, root element included */
+  int32_t n_features, n_groups;
+  int32_t max_len;              /* longest merged path (root included) */
+  const int64_t* path_offset;   /* [L+1] element range of each path */
+  const int32_t* feature;       /* [E] -1 for the root element, then ascending features */
+  const float* lower;           /* [E] bounds: an instance follows the path when */
+  const float* upper;           /* [E]   lower <= x[feature] < upper (root: -inf, +inf) */
+  const double* zero_fraction;  /* [E] z: product of cover ratios (root: 1) */
+  const double* v;              /* [L] leaf value */
+  const int32_t* group;         /* [L] output group */
+  const int32_t* tree;          /* [L] source tree */
+  const double* bias;           /* [G] phi_0 = sum_paths v * prod z + base_score */
+} gts_paths_view;
+
+/* Validate the model, extract one path per leaf (trees in input order, leaves in
+   DFS left-first order) and merge repeated features (bounds intersect, zero
+   fractions multiply in root-to-leaf order, fp64).  Errors: INVALID_ARGUMENT,
+   INVALID_MODEL, PATH_TOO_LONG, OUT_OF_MEMORY.  *out is set only on success. */
+gts_status gts_extract_paths(const gts_model* model, gts_paths** out);
+gts_status gts_paths_view_get(const gts_paths* paths, gts_paths_view* view);
+void gts_paths_free(gts_paths* paths);
+
+/* ----------------------------------------------------------------- (2) bins */
+
+typedef struct gts_bins gts_bins; /* opaque, library-owned; keeps its own reference to the paths */
+
+typedef struct gts_bins_view {
+  int64_t n_items;              /* = n_paths */
+  int64_t n_bins;               /* K */
+  int64_t sum_sizes;            /* sum of item sizes = n_elems */
+  int32_t capacity;             /* B */
+  int32_t algo;                 /* gts_pack_algo */
+  double utilisation;           /* sum_sizes / (capacity * K), 1.0 when K == 0 */
+  double pack_seconds;          /* wall time of the packing heuristic alone */
+  const int32_t* bin_of_path;   /* [L] bin index, bins numbered by creation */
+  const uint8_t* lane_of_path;  /* [L] first lane; a path occupies consecutive lanes */
+} gts_bins_view;
+
+/* Pack paths (item size = merged length incl. root) into bins of `capacity`
+   lanes (1..32; 32 in production).  FFD/BFD: items in non-increasing size,
+   ties by path index; FFD picks the lowest-index bin that fits, BFD the bin
+   with the smallest sufficient residual (ties: lowest index).  Errors:
+   INVALID_ARGUMENT (capacity, algo), PATH_TOO_LONG (an item > capacity). */
+gts_status gts_binpack(const gts_paths* paths, int32_t capacity, gts_pack_algo algo, gts_bins** out);
+gts_status gts_bins_view_get(const gts_bins* bins, gts_bins_view* view);
+void gts_bins_free(gts_bins* bins);
+
+/* ------------------------------------------------------------ device blob */
+
+/* Host-side description of a blob; plain old data, safe to memcpy / broadcast.
+   gts_shap needs it to configure the launch without reading device memory. */
+typedef struct gts_blob_info {
+  uint32_t magic;               /* 0x47545342 'GTSB' */
+  uint32_t abi_version;         /* GTS_ABI_VERSION */
+  int32_t dtype;                /* gts_dtype */
+  int32_t layout;               /* gts_layout */
+  int32_t n_features, n_groups;
+  int32_t max_slots;            /* NODAL: feature slots per chunk (16, 32 or 64) */
+  int32_t max_len;              /* longest merged path, root included */
+  int64_t n_paths, n_elems;
+  int64_t n_units;              /* NODAL: chunks; WARP_BINS: bins */
+  int64_t bytes;                /* total blob size */
+  double shap_flops_per_row;    /* algorithmic flops per row */
+  double inter_flops_per_row;
+  double paper_shap_flops_per_row;   /* SURVEY.md §8(d) F_shap, for context */
+  double paper_inter_flops_per_row;  /* SURVEY.md §8(d) F_int */
+  int64_t max_chunk_words;      /* NODAL: shared-memory staging needs of the largest chunk */
+  int64_t max_chunk_elems;
+  int64_t max_chunk_paths;
+  int64_t reserved[5];
+} gts_blob_info;
+
+/* Describe the blob for (bins, dtype, layout).  max_slots (NODAL only) is the
+   number of distinct features a chunk may touch, one of 16, 32, 64, or 0 for
+   the default (the smallest of them >= n_features, else 32).  Interactions
+   need max_slots <= 16 (shared-memory tile).  Errors: INVALID_ARGUMENT. */
+gts_status gts_blob_plan(const gts_bins* bins, gts_dtype dtype, gts_layout layout, int32_t max_slots,
+                         gts_blob_info* info);
+/* Serialise into caller HOST memory of at least info->bytes (any alignment
+   >= 16).  The caller copies the bytes to a device buffer (16-byte aligned). */
+gts_status gts_blob_write(const gts_bins* bins, const gts_blob_info* info, void* host_dst, size_t dst_bytes);
+
+/* ---------------------------------------------------------- (3)/(4) compute */
+
+/* SHAP values for rows [0, n_rows) of X.
+   d_blob:  device copy of the blob described by info.
+   d_X:     device, row-major [n_rows][ld_x] of info->dtype, ld_x >= n_features;
+            values finite (reading G17).
+   d_phi:   device [n_rows][n_groups][n_features+1] of info->dtype, fully
+            overwritten; column n_features holds the bias phi_0 (reading G14).
+   stream:  cudaStream_t (NULL = default stream).  n_rows == 0 is a no-op.   */
+gts_status gts_shap(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
+                    int64_t ld_x, void* d_phi, void* stream);
+
+/* SHAP interaction values; d_phi_ij: device
+   [n_rows][n_groups][n_features+1][n_features+1] of info->dtype, fully
+   overwritten: off-diagonal Eq. 3, diagonal Eq. 6, cell (M,M) = bias,
+   cells (i,M) and (M,i) = 0.  NODAL blobs need max_slots <= 16. */
+gts_status gts_shap_interactions(const gts_blob_info* info, const void* d_blob, const void* d_X,
+                                 int64_t n_rows, int64_t ld_x, void* d_phi_ij, void* stream);
+
+/* Number of kernel launches one gts_shap / gts_shap_interactions call issues. */
+int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions);
+
+const char* gts_last_error(void);
+const char* gts_status_string(gts_status status);
+int32_t gts_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GTS_H_ */

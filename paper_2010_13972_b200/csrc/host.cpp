@@ -1,0 +1,898 @@
+// host.cpp -- host side of the C ABI (include/gts.h): model validation, path
+// extraction + duplicate merge, bin packing, bias, blob serialisation.
+//
+// SURVEY.md §8(a) rows a1 (ingest + validate), a2 (extract + merge), a3 (bin
+// packing), a4 (device layout), a5 (bias).  Parallel over trees with OpenMP,
+// deterministic: per-tree results are concatenated in tree order.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <new>
+#include <set>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/gts.h"
+#include "blob_format.h"
+
+namespace gts {
+
+// ---------------------------------------------------------------- errors
+
+static thread_local std::string g_last_error;
+
+gts_status fail(gts_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+const char* last_error() { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------- path table
+
+struct PathTable {
+  int32_t n_features = 0, n_groups = 0, max_len = 0;
+  double base_score = 0.0;
+  std::vector<int64_t> path_offset;
+  std::vector<int32_t> feature;
+  std::vector<float> lower, upper;
+  std::vector<double> zero_fraction;
+  std::vector<double> v;
+  std::vector<int32_t> group, tree;
+  std::vector<double> bias;
+  int64_t n_paths() const { return (int64_t)v.size(); }
+  int64_t n_elems() const { return (int64_t)feature.size(); }
+  int32_t len(int64_t p) const { return (int32_t)(path_offset[p + 1] - path_offset[p]); }
+};
+
+}  // namespace gts
+
+struct gts_paths {
+  std::shared_ptr<gts::PathTable> tab;
+};
+
+struct gts_bins {
+  std::shared_ptr<gts::PathTable> tab;
+  int32_t capacity = 32;
+  int32_t algo = 0;
+  int64_t n_bins = 0;
+  int64_t sum_sizes = 0;
+  double pack_seconds = 0.0;
+  std::vector<int32_t> bin_of_path;
+  std::vector<uint8_t> lane_of_path;
+};
+
+namespace gts {
+
+// ----------------------------------------------------------- validation (a1)
+
+static gts_status validate_model(const gts_model* m) {
+  if (!m) return fail(GTS_ERR_INVALID_ARGUMENT, "model is NULL");
+  if (m->n_trees < 0) return fail(GTS_ERR_INVALID_ARGUMENT, "n_trees < 0");
+  if (m->n_features < 1) return fail(GTS_ERR_INVALID_ARGUMENT, "n_features < 1");
+  if (m->n_groups < 1) return fail(GTS_ERR_INVALID_ARGUMENT, "n_groups < 1");
+  if (!std::isfinite(m->base_score)) return fail(GTS_ERR_INVALID_MODEL, "base_score not finite");
+  if (m->n_trees == 0) return GTS_OK;
+  if (!m->node_offset || !m->left || !m->right || !m->feature || !m->threshold || !m->cover ||
+      !m->leaf_value || !m->tree_group)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "model array is NULL");
+  if (m->node_offset[0] != 0) return fail(GTS_ERR_INVALID_MODEL, "node_offset[0] != 0");
+  for (int64_t t = 0; t < m->n_trees; ++t) {
+    if (m->node_offset[t + 1] <= m->node_offset[t])
+      return fail(GTS_ERR_INVALID_MODEL, "tree %lld has no nodes", (long long)t);
+    if (m->node_offset[t + 1] - m->node_offset[t] > (int64_t)INT32_MAX)
+      return fail(GTS_ERR_INVALID_MODEL, "tree %lld too large", (long long)t);
+    if (m->tree_group[t] < 0 || m->tree_group[t] >= m->n_groups)
+      return fail(GTS_ERR_INVALID_MODEL, "tree %lld group %d out of range", (long long)t, m->tree_group[t]);
+  }
+  const int64_t T = m->n_trees;
+  std::vector<int> err_code(T, 0);
+  std::vector<std::string> err_msg(T);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t t = 0; t < T; ++t) {
+    const int64_t base = m->node_offset[t];
+    const int32_t n = (int32_t)(m->node_offset[t + 1] - base);
+    std::vector<uint8_t> parents(n, 0);
+    char buf[256];
+    auto bad = [&](const char* what, int32_t j) {
+      snprintf(buf, sizeof(buf), "tree %lld node %d: %s", (long long)t, j, what);
+      err_code[t] = 1;
+      err_msg[t] = buf;
+    };
+    for (int32_t j = 0; j < n && !err_code[t]; ++j) {
+      const int64_t g = base + j;
+      const double c = m->cover[g];
+      if (!(c > 0.0) || !std::isfinite(c)) { bad("cover must be finite and > 0", j); break; }
+      const int32_t a = m->left[g], b = m->right[g];
+      if (a < 0 && b < 0) {
+        if (!std::isfinite(m->leaf_value[g])) bad("leaf value not finite", j);
+        continue;
+      }
+      if (a <= 0 || b <= 0 || a >= n || b >= n || a == b) { bad("dangling or invalid child index", j); break; }
+      if (m->feature[g] < 0 || m->feature[g] >= m->n_features) { bad("feature out of range", j); break; }
+      if (!std::isfinite(m->threshold[g])) { bad("threshold not finite", j); break; }
+      if (++parents[a] > 1 || ++parents[b] > 1) { bad("node has more than one parent", j); break; }
+      const double sum = m->cover[base + a] + m->cover[base + b];
+      if (std::fabs(sum - c) > 1e-6 * c) { bad("cover(parent) != cover(left) + cover(right)", j); break; }
+    }
+    if (!err_code[t] && parents[0] != 0) bad("root has a parent (cycle)", 0);
+    for (int32_t j = 1; j < n && !err_code[t]; ++j)
+      if (parents[j] != 1) bad("node unreachable (no parent)", j);
+    if (!err_code[t]) {  // exactly-one-parent + all reachable from the root => a tree
+      std::vector<int32_t> st{0};
+      int32_t seen = 0;
+      while (!st.empty() && seen <= n) {
+        int32_t j = st.back();
+        st.pop_back();
+        ++seen;
+        if (m->left[base + j] >= 0) { st.push_back(m->left[base + j]); st.push_back(m->right[base + j]); }
+      }
+      if (seen != n) bad("cycle or unreachable nodes", 0);
+    }
+  }
+  for (int64_t t = 0; t < T; ++t)
+    if (err_code[t]) return fail(GTS_ERR_INVALID_MODEL, "%s", err_msg[t].c_str());
+  return GTS_OK;
+}
+
+// ------------------------------------------------- extraction + merge (a2)
+
+struct Edge {
+  int32_t f;
+  float lo, hi;
+  double z;
+};
+
+// Stable insertion sort by feature (paths are short), then merge runs of equal
+// features: lower = max, upper = min, z = product in root-to-leaf order
+// (reading G11).  Returns the merged count.
+static int merge_path(const Edge* raw, int n, Edge* out, Edge* scratch) {
+  for (int i = 0; i < n; ++i) {
+    Edge e = raw[i];
+    int j = i;
+    while (j > 0 && scratch[j - 1].f > e.f) { scratch[j] = scratch[j - 1]; --j; }
+    scratch[j] = e;
+  }
+  int m = 0;
+  for (int i = 0; i < n; ++i) {
+    const Edge& e = scratch[i];
+    if (m > 0 && out[m - 1].f == e.f) {
+      Edge& p = out[m - 1];
+      p.lo = std::max(p.lo, e.lo);
+      p.hi = std::min(p.hi, e.hi);
+      p.z = p.z * e.z;
+    } else {
+      out[m++] = e;
+    }
+  }
+  return m;
+}
+
+struct TreeOut {
+  std::vector<int32_t> len;  // merged length incl. root, per path
+  std::vector<Edge> elems;   // non-root merged elements, path after path
+  std::vector<double> v;
+  int32_t max_len = 0;
+};
+
+// One path per leaf, DFS left-first (reading G9).  Edge of the left child:
+// [-inf, t); right child: [t, +inf) (x < t -> left, reading G1); z = r_child / r_parent.
+static void extract_tree(const gts_model* m, int64_t t, TreeOut& out) {
+  const int64_t base = m->node_offset[t];
+  struct Item { int32_t node, depth; Edge edge; };
+  std::vector<Item> st;
+  std::vector<Edge> edges, merged, scratch;
+  st.push_back({0, 0, Edge{-1, 0.f, 0.f, 1.0}});
+  while (!st.empty()) {
+    Item it = st.back();
+    st.pop_back();
+    if (it.depth > 0) {
+      edges.resize(it.depth - 1);
+      edges.push_back(it.edge);
+    }
+    const int64_t g = base + it.node;
+    const int32_t a = m->left[g], b = m->right[g];
+    if (a < 0) {
+      const int d = it.depth;
+      merged.resize(d + 1);
+      scratch.resize(d + 1);
+      const int k = merge_path(edges.data(), d, merged.data(), scratch.data());
+      out.len.push_back(k + 1);
+      out.max_len = std::max(out.max_len, k + 1);
+      out.elems.insert(out.elems.end(), merged.begin(), merged.begin() + k);
+      out.v.push_back(m->leaf_value[g]);
+      continue;
+    }
+    const float thr = m->threshold[g];
+    const int32_t f = m->feature[g];
+    const double rj = m->cover[g];
+    const float inf = std::numeric_limits<float>::infinity();
+    st.push_back({b, it.depth + 1, Edge{f, thr, inf, m->cover[base + b] / rj}});
+    st.push_back({a, it.depth + 1, Edge{f, -inf, thr, m->cover[base + a] / rj}});
+  }
+}
+
+static gts_status extract(const gts_model* m, std::shared_ptr<PathTable>& out) {
+  gts_status st = validate_model(m);
+  if (st != GTS_OK) return st;
+  auto tab = std::make_shared<PathTable>();
+  tab->n_features = m->n_features;
+  tab->n_groups = m->n_groups;
+  tab->base_score = m->base_score;
+  const int64_t T = m->n_trees;
+  std::vector<TreeOut> trees(T);
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int64_t t = 0; t < T; ++t) extract_tree(m, t, trees[t]);
+  int64_t L = 0, E = 0;
+  std::vector<int64_t> path_base(T + 1, 0), elem_base(T + 1, 0);
+  for (int64_t t = 0; t < T; ++t) {
+    path_base[t + 1] = path_base[t] + (int64_t)trees[t].v.size();
+    elem_base[t + 1] = elem_base[t] + (int64_t)trees[t].elems.size() + (int64_t)trees[t].v.size();
+    tab->max_len = std::max(tab->max_len, trees[t].max_len);
+  }
+  L = path_base[T];
+  E = elem_base[T];
+  if (tab->max_len > kWarp)
+    return fail(GTS_ERR_PATH_TOO_LONG, "merged path length %d exceeds the warp size %d (PAPER.md:215)",
+                tab->max_len, kWarp);
+  tab->path_offset.resize(L + 1);
+  tab->feature.resize(E);
+  tab->lower.resize(E);
+  tab->upper.resize(E);
+  tab->zero_fraction.resize(E);
+  tab->v.resize(L);
+  tab->group.resize(L);
+  tab->tree.resize(L);
+  const float inf = std::numeric_limits<float>::infinity();
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int64_t t = 0; t < T; ++t) {
+    const TreeOut& tr = trees[t];
+    int64_t p = path_base[t], e = elem_base[t];
+    size_t src = 0;
+    for (size_t q = 0; q < tr.v.size(); ++q, ++p) {
+      tab->path_offset[p] = e;
+      tab->feature[e] = -1;  // root element (Listing 1: "-1 is root"; reading G2)
+      tab->lower[e] = -inf;
+      tab->upper[e] = inf;
+      tab->zero_fraction[e] = 1.0;
+      ++e;
+      for (int32_t i = 1; i < tr.len[q]; ++i, ++e, ++src) {
+        const Edge& x = tr.elems[src];
+        tab->feature[e] = x.f;
+        tab->lower[e] = x.lo;
+        tab->upper[e] = x.hi;
+        tab->zero_fraction[e] = x.z;
+      }
+      tab->v[p] = tr.v[q];
+      tab->group[p] = m->tree_group[t];
+      tab->tree[p] = (int32_t)t;
+    }
+  }
+  tab->path_offset[L] = E;
+  // bias (a5, reading G13): sum over paths in path order of v * prod z (table
+  // order), fp64; base_score added last.
+  tab->bias.assign(m->n_groups, 0.0);
+  for (int64_t p = 0; p < L; ++p) {
+    double prod = 1.0;
+    for (int64_t e = tab->path_offset[p]; e < tab->path_offset[p + 1]; ++e) prod *= tab->zero_fraction[e];
+    tab->bias[tab->group[p]] += tab->v[p] * prod;
+  }
+  for (int32_t g = 0; g < m->n_groups; ++g) tab->bias[g] += m->base_score;
+  out = std::move(tab);
+  return GTS_OK;
+}
+
+// -------------------------------------------------------- bin packing (a3)
+
+// Items in non-increasing size, ties by index (counting sort, stable).
+static std::vector<int64_t> decreasing_order(const std::vector<int32_t>& size, int32_t cap) {
+  std::vector<int64_t> count(cap + 2, 0);
+  for (int32_t s : size) count[s]++;
+  std::vector<int64_t> start(cap + 2, 0);
+  int64_t pos = 0;
+  for (int32_t s = cap; s >= 1; --s) { start[s] = pos; pos += count[s]; }
+  std::vector<int64_t> order(size.size());
+  for (int64_t i = 0; i < (int64_t)size.size(); ++i) order[start[size[i]]++] = i;
+  return order;
+}
+
+// FFD with a max-segment-tree over bin residuals packed into an array
+// (PAPER.md:526).  Unopened bins have residual = capacity and lie after the
+// opened ones, so "first leaf with residual >= s" is either the first opened bin
+// that fits or the next new bin.
+static int64_t pack_ffd(const std::vector<int32_t>& size, int32_t cap, std::vector<int32_t>& bin_of) {
+  const int64_t n = (int64_t)size.size();
+  int64_t leaves = 1;
+  while (leaves < std::max<int64_t>(n, 1)) leaves <<= 1;
+  std::vector<int32_t> tree(2 * leaves, cap);
+  int64_t n_bins = 0;
+  for (int64_t i : decreasing_order(size, cap)) {
+    const int32_t s = size[i];
+    int64_t node = 1;
+    while (node < leaves) node = (tree[2 * node] >= s) ? 2 * node : 2 * node + 1;
+    const int64_t b = node - leaves;
+    if (b >= n_bins) n_bins = b + 1;
+    bin_of[i] = (int32_t)b;
+    tree[node] -= s;
+    for (node >>= 1; node >= 1; node >>= 1) tree[node] = std::max(tree[2 * node], tree[2 * node + 1]);
+  }
+  return n_bins;
+}
+
+// BFD with an ordered set of (residual, bin) ("implemented easily
+// using std::set"); lower_bound gives the smallest residual >= s, lowest bin id.
+static int64_t pack_bfd(const std::vector<int32_t>& size, int32_t cap, std::vector<int32_t>& bin_of) {
+  std::set<std::pair<int32_t, int64_t>> open;
+  int64_t n_bins = 0;
+  for (int64_t i : decreasing_order(size, cap)) {
+    const int32_t s = size[i];
+    auto it = open.lower_bound({s, (int64_t)-1});
+    int64_t b;
+    int32_t res;
+    if (it == open.end()) {
+      b = n_bins++;
+      res = cap - s;
+    } else {
+      b = it->second;
+      res = it->first - s;
+      open.erase(it);
+    }
+    if (res > 0) open.insert({res, b});
+    bin_of[i] = (int32_t)b;
+  }
+  return n_bins;
+}
+
+static int64_t pack_nf(const std::vector<int32_t>& size, int32_t cap, std::vector<int32_t>& bin_of) {
+  int64_t n_bins = 0;
+  int32_t fill = cap + 1;
+  for (size_t i = 0; i < size.size(); ++i) {
+    if (fill + size[i] > cap) { ++n_bins; fill = 0; }
+    bin_of[i] = (int32_t)(n_bins - 1);
+    fill += size[i];
+  }
+  return n_bins;
+}
+
+static gts_status binpack(const std::shared_ptr<PathTable>& tab, int32_t cap, int32_t algo, gts_bins& out) {
+  if (cap < 1 || cap > kWarp) return fail(GTS_ERR_INVALID_ARGUMENT, "capacity %d not in [1, %d]", cap, kWarp);
+  if (algo < GTS_PACK_FFD || algo > GTS_PACK_NONE) return fail(GTS_ERR_INVALID_ARGUMENT, "bad pack algo %d", algo);
+  const int64_t L = tab->n_paths();
+  std::vector<int32_t> size(L);
+  for (int64_t p = 0; p < L; ++p) {
+    size[p] = tab->len(p);
+    if (size[p] > cap)
+      return fail(GTS_ERR_PATH_TOO_LONG, "path %lld of length %d exceeds capacity %d", (long long)p, size[p], cap);
+  }
+  out.tab = tab;
+  out.capacity = cap;
+  out.algo = algo;
+  out.bin_of_path.assign(L, 0);
+  out.lane_of_path.assign(L, 0);
+  auto t0 = std::chrono::steady_clock::now();
+  int64_t K = 0;
+  switch (algo) {
+    case GTS_PACK_FFD: K = pack_ffd(size, cap, out.bin_of_path); break;
+    case GTS_PACK_BFD: K = pack_bfd(size, cap, out.bin_of_path); break;
+    case GTS_PACK_NF: K = pack_nf(size, cap, out.bin_of_path); break;
+    default:
+      for (int64_t p = 0; p < L; ++p) out.bin_of_path[p] = (int32_t)p;
+      K = L;
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  out.pack_seconds = std::chrono::duration<double>(t1 - t0).count();
+  out.n_bins = K;
+  // lanes: consecutive, in insertion order (FFD/BFD: decreasing order; NF/none: path order)
+  std::vector<int32_t> fill(K, 0);
+  if (algo == GTS_PACK_FFD || algo == GTS_PACK_BFD) {
+    for (int64_t i : decreasing_order(size, cap)) {
+      out.lane_of_path[i] = (uint8_t)fill[out.bin_of_path[i]];
+      fill[out.bin_of_path[i]] += size[i];
+    }
+  } else {
+    for (int64_t i = 0; i < L; ++i) {
+      out.lane_of_path[i] = (uint8_t)fill[out.bin_of_path[i]];
+      fill[out.bin_of_path[i]] += size[i];
+    }
+  }
+  out.sum_sizes = tab->n_elems();
+  return GTS_OK;
+}
+
+// --------------------------------------------------------- Gauss-Legendre
+
+// Nodes t_q in (0,1) ascending and weights w_q (sum 1) of the Q-point
+// Gauss-Legendre rule on [0,1]; exact for polynomials of degree <= 2Q-1.
+// Newton iteration on P_Q in long double.
+static void gauss_legendre01(int Q, long double* t, long double* w) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int i = 0; i < Q; ++i) {
+    long double x = std::cos(pi * (i + 0.75L) / (Q + 0.5L));
+    long double dp = 0;
+    for (int it = 0; it < 100; ++it) {
+      long double p0 = 1, p1 = x;
+      for (int n = 2; n <= Q; ++n) {
+        long double p2 = ((2 * n - 1) * x * p1 - (n - 1) * p0) / n;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (Q == 1) { p1 = x; p0 = 1; }
+      dp = Q * (x * p1 - p0) / (x * x - 1);
+      long double dx = p1 / dp;
+      x -= dx;
+      if (std::fabs((double)dx) < 1e-19) break;
+    }
+    {  // recompute derivative at the converged root
+      long double p0 = 1, p1 = x;
+      for (int n = 2; n <= Q; ++n) {
+        long double p2 = ((2 * n - 1) * x * p1 - (n - 1) * p0) / n;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = Q * (x * p1 - p0) / (x * x - 1);
+    }
+    // x descending in i -> t = (1 - x)/2 ascending
+    t[i] = (1 - x) / 2;
+    w[i] = 1 / ((1 - x * x) * dp * dp);  // (2 / ((1-x^2) P'^2)) / 2
+  }
+}
+
+// ------------------------------------------------------------ blobs (a4)
+
+static int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+struct NodalPlan {
+  std::vector<ChunkRec> chunks;
+  std::vector<int32_t> slotmap;
+  std::vector<PathRec> paths;
+  std::vector<ElemRec> elems;
+  std::vector<double> work_shap, work_inter;
+  int64_t max_words = 0, max_elems = 0, max_paths = 0;
+};
+
+static int pick_slots(int32_t requested, int32_t M) {
+  if (requested != 0) return requested;
+  if (M <= 16) return 16;
+  if (M <= 32) return 32;
+  if (M <= 64) return 64;
+  return 32;  // wide models: per-chunk slot maps
+}
+
+// nodal op counts per (row, path), DESIGN.md §6
+static double nodal_shap_flops(int k, int q) { return 3.0 * k * q + 3.0 * k + 2.0 * q; }
+static double nodal_inter_flops(int k, int q) {
+  return (double)k * (k - 1) * q + 7.0 * k * q + q + 2.0 * k + 0.5 * k * (k + 1);
+}
+static double paper_shap_flops(int k) { return 5.5 * k * k + 7.5 * k; }
+static double paper_inter_flops(int k) { return paper_shap_flops(k) + (double)k * (k - 1) * (5.5 * k + 1) + 2.0 * k; }
+
+static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np) {
+  const int32_t M = tab.n_features;
+  const bool identity = M <= S;
+  const int64_t L = tab.n_paths();
+  // paths grouped by group, input order within a group
+  std::vector<int64_t> order;
+  order.reserve(L);
+  for (int32_t g = 0; g < tab.n_groups; ++g)
+    for (int64_t p = 0; p < L; ++p)
+      if (tab.group[p] == g && tab.len(p) > 1) order.push_back(p);
+  const int64_t max_words = kChunkTableBytes / (int64_t)tsize;
+  int32_t map_id = -1;
+  std::vector<int32_t> cur_map;  // sorted features of the current chunk (non-identity)
+  size_t i = 0;
+  while (i < order.size()) {
+    ChunkRec c{};
+    c.group = tab.group[order[i]];
+    c.path_begin = (int64_t)np.paths.size();
+    c.elem_begin = (int64_t)np.elems.size();
+    std::vector<int32_t> feats;
+    std::vector<int64_t> members;
+    int64_t words = 0, nel = 0;
+    size_t j = i;
+    while (j < order.size() && (int)members.size() < kMaxChunkPaths) {
+      const int64_t p = order[j];
+      if (tab.group[p] != c.group) break;
+      const int k = tab.len(p) - 1, q = (k + 1) / 2;
+      const int64_t w = nodal_path_words(k, q);
+      if (!members.empty() && words + w > max_words) break;
+      if (!identity) {
+        std::vector<int32_t> u = feats;
+        for (int64_t e = tab.path_offset[p] + 1; e < tab.path_offset[p + 1]; ++e) u.push_back(tab.feature[e]);
+        std::sort(u.begin(), u.end());
+        u.erase(std::unique(u.begin(), u.end()), u.end());
+        if (!members.empty() && (int)u.size() > S) break;
+        feats.swap(u);
+      }
+      members.push_back(p);
+      words += w;
+      nel += k;
+      ++j;
+    }
+    if (identity) {
+      feats.resize(M);
+      for (int32_t f = 0; f < M; ++f) feats[f] = f;
+    }
+    // stable order by q descending inside the chunk (template locality)
+    std::stable_sort(members.begin(), members.end(), [&](int64_t a, int64_t b) {
+      return (tab.len(a) / 2) > (tab.len(b) / 2);
+    });
+    if (feats != cur_map || map_id < 0) {
+      ++map_id;
+      cur_map = feats;
+      c.slotmap_begin = (int64_t)np.slotmap.size();
+      np.slotmap.insert(np.slotmap.end(), feats.begin(), feats.end());
+    } else {
+      c.slotmap_begin = np.chunks.back().slotmap_begin;
+    }
+    c.map_id = map_id;
+    c.n_slots = (int32_t)feats.size();
+    c.n_paths = (int32_t)members.size();
+    c.n_elems = (int32_t)nel;
+    int32_t table = 0, rel = 0, maxq = 0;
+    double ws = 0, wi = 0;
+    for (int64_t p : members) {
+      const int k = tab.len(p) - 1, q = (k + 1) / 2;
+      PathRec pr{};
+      pr.k = k;
+      pr.q = q;
+      pr.elem = rel;
+      pr.table = table;
+      pr.v = tab.v[p];
+      np.paths.push_back(pr);
+      for (int64_t e = tab.path_offset[p] + 1; e < tab.path_offset[p + 1]; ++e) {
+        ElemRec er{};
+        const int32_t f = tab.feature[e];
+        er.slot = (int32_t)(std::lower_bound(feats.begin(), feats.end(), f) - feats.begin());
+        er.lo = tab.lower[e];
+        er.hi = tab.upper[e];
+        er.z = tab.zero_fraction[e];
+        np.elems.push_back(er);
+      }
+      rel += k;
+      table += nodal_path_words(k, q);
+      maxq = std::max(maxq, q);
+      ws += nodal_shap_flops(k, q);
+      wi += nodal_inter_flops(k, q);
+    }
+    c.table_words = table;
+    c.max_q = maxq;
+    np.max_words = std::max<int64_t>(np.max_words, table);
+    np.max_elems = std::max<int64_t>(np.max_elems, nel);
+    np.max_paths = std::max<int64_t>(np.max_paths, c.n_paths);
+    np.chunks.push_back(c);
+    np.work_shap.push_back(ws);
+    np.work_inter.push_back(wi);
+    i = j;
+  }
+}
+
+struct BinsPlan {
+  std::vector<int64_t> bin_order;  // device bin -> packer bin, k_max descending
+  std::vector<int32_t> kmax;
+};
+
+static void plan_bins(const gts_bins& b, BinsPlan& bp) {
+  const PathTable& tab = *b.tab;
+  std::vector<int32_t> km(b.n_bins, 0);
+  for (int64_t p = 0; p < tab.n_paths(); ++p)
+    km[b.bin_of_path[p]] = std::max(km[b.bin_of_path[p]], tab.len(p) - 1);
+  bp.bin_order.resize(b.n_bins);
+  for (int64_t i = 0; i < b.n_bins; ++i) bp.bin_order[i] = i;
+  std::stable_sort(bp.bin_order.begin(), bp.bin_order.end(), [&](int64_t x, int64_t y) { return km[x] > km[y]; });
+  bp.kmax.resize(b.n_bins);
+  for (int64_t i = 0; i < b.n_bins; ++i) bp.kmax[i] = km[bp.bin_order[i]];
+}
+
+static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, int32_t max_slots,
+                            gts_blob_info* info, BlobHeader* hdr, NodalPlan* np, BinsPlan* bp) {
+  if (!b || !info) return fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (dtype != GTS_F32 && dtype != GTS_F64) return fail(GTS_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
+  if (layout != GTS_LAYOUT_NODAL && layout != GTS_LAYOUT_WARP_BINS)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "bad layout %d", layout);
+  if (max_slots != 0 && max_slots != 16 && max_slots != 32 && max_slots != 64)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "max_slots must be 0, 16, 32 or 64");
+  const PathTable& tab = *b->tab;
+  const size_t tsize = dtype == GTS_F32 ? 4 : 8;
+  BlobHeader h{};
+  h.magic = kMagic;
+  h.version = GTS_ABI_VERSION;
+  h.dtype = dtype;
+  h.layout = layout;
+  h.n_features = tab.n_features;
+  h.n_groups = tab.n_groups;
+  h.max_len = tab.max_len;
+  h.n_paths = tab.n_paths();
+  h.n_elems = tab.n_elems();
+  int64_t off = align256(sizeof(BlobHeader));
+  h.off_bias = off;
+  off = align256(off + 8 * (int64_t)tab.n_groups);
+  double fs = 0, fi = 0, ps = 0, pi = 0;
+  for (int64_t p = 0; p < tab.n_paths(); ++p) {
+    const int k = tab.len(p) - 1, q = (k + 1) / 2;
+    if (k == 0) continue;
+    fs += nodal_shap_flops(k, q);
+    fi += nodal_inter_flops(k, q);
+    ps += paper_shap_flops(k);
+    pi += paper_inter_flops(k);
+  }
+  if (layout == GTS_LAYOUT_NODAL) {
+    int S = pick_slots(max_slots, tab.n_features);
+    const int max_k = std::max(tab.max_len - 1, 0);
+    if (max_slots == 0) {
+      while (S < max_k && S < 64) S *= 2;
+    } else if (S < max_k && S < tab.n_features) {
+      return fail(GTS_ERR_INVALID_ARGUMENT,
+                  "max_slots %d is smaller than the %d features of the longest path", S, max_k);
+    }
+    h.max_slots = S;
+    NodalPlan local;
+    NodalPlan& P = np ? *np : local;
+    plan_nodal(tab, S, tsize, P);
+    h.n_units = (int64_t)P.chunks.size();
+    h.n_kept_paths = (int64_t)P.paths.size();
+    h.n_kept_elems = (int64_t)P.elems.size();
+    h.max_chunk_words = P.max_words;
+    h.max_chunk_elems = P.max_elems;
+    h.max_chunk_paths = P.max_paths;
+    h.off_gauss = off;
+    off = align256(off + (int64_t)tsize * kQMax * 3 * kQMax);
+    h.off_units = off;
+    off = align256(off + (int64_t)sizeof(ChunkRec) * h.n_units);
+    h.off_work = off;
+    off = align256(off + 8 * 2 * (h.n_units + 1));
+    h.off_slotmap = off;
+    off = align256(off + 4 * (int64_t)P.slotmap.size());
+    h.off_paths = off;
+    off = align256(off + (int64_t)sizeof(PathRec) * h.n_kept_paths);
+    h.off_elems = off;
+    off = align256(off + (int64_t)sizeof(ElemRec) * h.n_kept_elems);
+  } else {
+    h.max_slots = 0;
+    h.n_units = b->n_bins;
+    if (b->capacity != kWarp)
+      return fail(GTS_ERR_INVALID_ARGUMENT, "WARP_BINS layout needs capacity %d packing", kWarp);
+    BinsPlan local;
+    BinsPlan& P = bp ? *bp : local;
+    plan_bins(*b, P);
+    h.off_units = off;
+    off = align256(off + 4 * h.n_units);
+    h.off_elems = off;
+    const int64_t lanes = h.n_units * kWarp;
+    off = align256(off + lanes * (4 + 4 + 4 + 4 + 4) + lanes * 2 * (int64_t)tsize);
+  }
+  h.bytes = off;
+  std::memset(info, 0, sizeof(*info));
+  info->magic = kMagic;
+  info->abi_version = GTS_ABI_VERSION;
+  info->dtype = dtype;
+  info->layout = layout;
+  info->n_features = tab.n_features;
+  info->n_groups = tab.n_groups;
+  info->max_slots = h.max_slots;
+  info->max_len = tab.max_len;
+  info->n_paths = h.n_paths;
+  info->n_elems = h.n_elems;
+  info->n_units = h.n_units;
+  info->bytes = h.bytes;
+  info->shap_flops_per_row = fs;
+  info->inter_flops_per_row = fi;
+  info->paper_shap_flops_per_row = ps;
+  info->paper_inter_flops_per_row = pi;
+  info->max_chunk_words = h.max_chunk_words;
+  info->max_chunk_elems = h.max_chunk_elems;
+  info->max_chunk_paths = h.max_chunk_paths;
+  if (hdr) *hdr = h;
+  return GTS_OK;
+}
+
+template <typename T>
+static void write_gauss(char* dst) {
+  T* g = reinterpret_cast<T*>(dst);
+  for (int Q = 1; Q <= kQMax; ++Q) {
+    long double t[kQMax], w[kQMax];
+    gauss_legendre01(Q, t, w);
+    T* row = g + (size_t)(Q - 1) * 3 * kQMax;
+    for (int q = 0; q < kQMax; ++q) {
+      row[q] = q < Q ? (T)t[q] : (T)0;
+      row[kQMax + q] = q < Q ? (T)w[q] : (T)0;
+      row[2 * kQMax + q] = q < Q ? (T)(-1.0L / (1.0L - t[q])) : (T)0;
+    }
+  }
+}
+
+template <typename T>
+static void write_bins(const gts_bins& b, const BinsPlan& bp, const BlobHeader& h, char* dst) {
+  const PathTable& tab = *b.tab;
+  const int64_t K = h.n_units, lanes = K * kWarp;
+  std::memcpy(dst + h.off_units, bp.kmax.data(), 4 * K);
+  char* base = dst + h.off_elems;
+  int32_t* feat = reinterpret_cast<int32_t*>(base);
+  int32_t* meta = feat + lanes;
+  int32_t* grp = meta + lanes;
+  float* lo = reinterpret_cast<float*>(grp + lanes);
+  float* hi = lo + lanes;
+  T* z = reinterpret_cast<T*>(hi + lanes);
+  T* v = z + lanes;
+  std::vector<int64_t> dev_of(K);
+  for (int64_t i = 0; i < K; ++i) dev_of[bp.bin_order[i]] = i;
+  const float inf = std::numeric_limits<float>::infinity();
+  for (int64_t l = 0; l < lanes; ++l) {
+    feat[l] = -2;
+    meta[l] = 0;
+    grp[l] = 0;
+    lo[l] = -inf;
+    hi[l] = inf;
+    z[l] = (T)1;
+    v[l] = (T)0;
+  }
+  for (int64_t p = 0; p < tab.n_paths(); ++p) {
+    const int64_t db = dev_of[b.bin_of_path[p]];
+    const int32_t lane0 = b.lane_of_path[p];
+    const int32_t len = tab.len(p);
+    for (int32_t r = 0; r < len; ++r) {
+      const int64_t e = tab.path_offset[p] + r;
+      const int64_t l = db * kWarp + lane0 + r;
+      feat[l] = tab.feature[e];
+      meta[l] = r | ((len - 1) << 8) | (lane0 << 16);
+      grp[l] = tab.group[p];
+      lo[l] = tab.lower[e];
+      hi[l] = tab.upper[e];
+      z[l] = (T)tab.zero_fraction[e];
+      v[l] = (T)tab.v[p];
+    }
+  }
+}
+
+static gts_status blob_write(const gts_bins* b, const gts_blob_info* info, void* dst, size_t dst_bytes) {
+  if (!b || !info || !dst) return fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
+  BlobHeader h;
+  NodalPlan np;
+  BinsPlan bp;
+  gts_blob_info fresh;
+  gts_status st = blob_plan(b, info->dtype, info->layout, info->max_slots, &fresh, &h, &np, &bp);
+  if (st != GTS_OK) return st;
+  if (fresh.bytes != info->bytes || fresh.n_units != info->n_units)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "blob info does not match these bins");
+  if (dst_bytes < (size_t)h.bytes)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "destination too small: %zu < %lld", dst_bytes, (long long)h.bytes);
+  char* out = static_cast<char*>(dst);
+  std::memset(out, 0, (size_t)h.bytes);
+  std::memcpy(out, &h, sizeof(h));
+  std::memcpy(out + h.off_bias, b->tab->bias.data(), 8 * b->tab->bias.size());
+  if (h.layout == GTS_LAYOUT_NODAL) {
+    if (h.dtype == GTS_F32) write_gauss<float>(out + h.off_gauss);
+    else write_gauss<double>(out + h.off_gauss);
+    std::memcpy(out + h.off_units, np.chunks.data(), sizeof(ChunkRec) * np.chunks.size());
+    double* ws = reinterpret_cast<double*>(out + h.off_work);
+    double* wi = ws + (h.n_units + 1);
+    ws[0] = wi[0] = 0;
+    for (int64_t c = 0; c < h.n_units; ++c) {
+      ws[c + 1] = ws[c] + np.work_shap[c];
+      wi[c + 1] = wi[c] + np.work_inter[c];
+    }
+    std::memcpy(out + h.off_slotmap, np.slotmap.data(), 4 * np.slotmap.size());
+    std::memcpy(out + h.off_paths, np.paths.data(), sizeof(PathRec) * np.paths.size());
+    std::memcpy(out + h.off_elems, np.elems.data(), sizeof(ElemRec) * np.elems.size());
+  } else {
+    if (h.dtype == GTS_F32) write_bins<float>(*b, bp, h, out);
+    else write_bins<double>(*b, bp, h, out);
+  }
+  return GTS_OK;
+}
+
+}  // namespace gts
+
+// ================================================================ C ABI
+
+extern "C" {
+
+gts_status gts_extract_paths(const gts_model* model, gts_paths** out) {
+  if (!out) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "out is NULL");
+  try {
+    std::shared_ptr<gts::PathTable> tab;
+    gts_status st = gts::extract(model, tab);
+    if (st != GTS_OK) return st;
+    *out = new gts_paths{std::move(tab)};
+    return GTS_OK;
+  } catch (const std::bad_alloc&) {
+    return gts::fail(GTS_ERR_OUT_OF_MEMORY, "out of host memory");
+  }
+}
+
+gts_status gts_paths_view_get(const gts_paths* paths, gts_paths_view* v) {
+  if (!paths || !v) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
+  const gts::PathTable& t = *paths->tab;
+  v->n_paths = t.n_paths();
+  v->n_elems = t.n_elems();
+  v->n_features = t.n_features;
+  v->n_groups = t.n_groups;
+  v->max_len = t.max_len;
+  v->path_offset = t.path_offset.data();
+  v->feature = t.feature.data();
+  v->lower = t.lower.data();
+  v->upper = t.upper.data();
+  v->zero_fraction = t.zero_fraction.data();
+  v->v = t.v.data();
+  v->group = t.group.data();
+  v->tree = t.tree.data();
+  v->bias = t.bias.data();
+  return GTS_OK;
+}
+
+void gts_paths_free(gts_paths* paths) { delete paths; }
+
+gts_status gts_binpack(const gts_paths* paths, int32_t capacity, gts_pack_algo algo, gts_bins** out) {
+  if (!paths || !out) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
+  try {
+    auto b = std::make_unique<gts_bins>();
+    gts_status st = gts::binpack(paths->tab, capacity, (int32_t)algo, *b);
+    if (st != GTS_OK) return st;
+    *out = b.release();
+    return GTS_OK;
+  } catch (const std::bad_alloc&) {
+    return gts::fail(GTS_ERR_OUT_OF_MEMORY, "out of host memory");
+  }
+}
+
+gts_status gts_bins_view_get(const gts_bins* b, gts_bins_view* v) {
+  if (!b || !v) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
+  v->n_items = (int64_t)b->bin_of_path.size();
+  v->n_bins = b->n_bins;
+  v->sum_sizes = b->sum_sizes;
+  v->capacity = b->capacity;
+  v->algo = b->algo;
+  v->utilisation = b->n_bins == 0 ? 1.0 : (double)b->sum_sizes / ((double)b->capacity * (double)b->n_bins);
+  v->pack_seconds = b->pack_seconds;
+  v->bin_of_path = b->bin_of_path.data();
+  v->lane_of_path = b->lane_of_path.data();
+  return GTS_OK;
+}
+
+void gts_bins_free(gts_bins* b) { delete b; }
+
+gts_status gts_blob_plan(const gts_bins* bins, gts_dtype dtype, gts_layout layout, int32_t max_slots,
+                         gts_blob_info* info) {
+  try {
+    return gts::blob_plan(bins, (int32_t)dtype, (int32_t)layout, max_slots, info, nullptr, nullptr, nullptr);
+  } catch (const std::bad_alloc&) {
+    return gts::fail(GTS_ERR_OUT_OF_MEMORY, "out of host memory");
+  }
+}
+
+gts_status gts_blob_write(const gts_bins* bins, const gts_blob_info* info, void* host_dst, size_t dst_bytes) {
+  try {
+    return gts::blob_write(bins, info, host_dst, dst_bytes);
+  } catch (const std::bad_alloc&) {
+    return gts::fail(GTS_ERR_OUT_OF_MEMORY, "out of host memory");
+  }
+}
+
+const char* gts_last_error(void) { return gts::last_error(); }
+
+const char* gts_status_string(gts_status s) {
+  switch (s) {
+    case GTS_OK: return "GTS_OK";
+    case GTS_ERR_INVALID_ARGUMENT: return "GTS_ERR_INVALID_ARGUMENT";
+    case GTS_ERR_INVALID_MODEL: return "GTS_ERR_INVALID_MODEL";
+    case GTS_ERR_PATH_TOO_LONG: return "GTS_ERR_PATH_TOO_LONG";
+    case GTS_ERR_NONFINITE: return "GTS_ERR_NONFINITE";
+    case GTS_ERR_CUDA: return "GTS_ERR_CUDA";
+    case GTS_ERR_OUT_OF_MEMORY: return "GTS_ERR_OUT_OF_MEMORY";
+  }
+  return "GTS_UNKNOWN_STATUS";
+}
+
+int32_t gts_abi_version(void) { return GTS_ABI_VERSION; }
+
+}  // extern "C"

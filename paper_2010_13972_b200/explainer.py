@@ -1,0 +1,121 @@
+"""Public Python API: a model-bound explainer over the C ABI.
+
+PyTorch provides device memory, streams and process groups only; every step of
+the hot path runs in libgts.so.  Preprocessing (extract -> pack -> blob) runs
+once per model and is amortised over all rows.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import gts
+
+_DT = {"f32": (gts.GTS_F32, torch.float32, np.float32), "f64": (gts.GTS_F64, torch.float64, np.float64)}
+
+
+class Blob:
+    """A serialised path table resident on one device (plus its host-side info)."""
+
+    def __init__(self, info: gts.gts_blob_info, device_bytes: torch.Tensor):
+        self.info = info
+        self.data = device_bytes
+
+    @property
+    def ptr(self) -> int:
+        return self.data.data_ptr()
+
+    @classmethod
+    def from_bins(cls, bins: gts.Bins, dtype: int, layout, max_slots: int, device) -> "Blob":
+        info = gts.gts_blob_plan(bins, dtype, layout, max_slots)
+        host = torch.empty(info.bytes, dtype=torch.uint8, pin_memory=torch.cuda.is_available())
+        gts.gts_blob_write(bins, info, host.numpy())
+        dev = host.to(device, non_blocking=True) if device is not None else host
+        return cls(info, dev)
+
+    def broadcast(self, src: int = 0, group=None) -> "Blob":
+        """Replicate this rank's blob to all ranks: ONE broadcast of the bytes
+        (NCCL over NVLink on GPUs), preceded by the small info record."""
+        import torch.distributed as dist
+        dev = self.data.device
+        meta = torch.zeros(256, dtype=torch.uint8, device=dev)
+        if dist.get_rank(group) == src:
+            raw = np.frombuffer(self.info.to_bytes(), np.uint8)
+            meta[:len(raw)] = torch.from_numpy(raw.copy()).to(dev)
+        dist.broadcast(meta, src, group=group)
+        info = gts.gts_blob_info.from_bytes(meta.cpu().numpy().tobytes())
+        if dist.get_rank(group) != src:
+            self.data = torch.empty(info.bytes, dtype=torch.uint8, device=dev)
+        dist.broadcast(self.data, src, group=group)
+        self.info = info
+        return self
+
+
+class TreeShapExplainer:
+    """Exact path-wise TreeShap for one tree ensemble.
+
+    model: any object with the gts_model fields (see include/gts.h).
+    dtype: "f32" (default) or "f64".  pack: "bfd" (default), "ffd", "nf", "none".
+    layout: "nodal" (B200-native default) or "warp_bins" (paper lineage).
+    """
+
+    def __init__(self, model, dtype: str = "f32", pack: str = "bfd", layout: str = "nodal",
+                 device=None, max_slots: int = 0, interactions: bool = True, build_blobs: bool = True):
+        self.dtype_code, self.torch_dtype, self.np_dtype = _DT[dtype]
+        self.layout = gts.LAYOUTS[layout] if isinstance(layout, str) else int(layout)
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None)
+        self.n_features = int(model.n_features)
+        self.n_groups = int(model.n_groups)
+        self.paths = gts.gts_extract_paths(model)
+        self.bins = gts.gts_binpack(self.paths, 32, pack)
+        self.blob = self.blob_int = None
+        if build_blobs:
+            self.blob = Blob.from_bins(self.bins, self.dtype_code, self.layout, max_slots, self.device)
+            if interactions:
+                if self.layout == gts.GTS_LAYOUT_NODAL and self.blob.info.max_slots != 16:
+                    self.blob_int = Blob.from_bins(self.bins, self.dtype_code, self.layout, 16, self.device)
+                else:
+                    self.blob_int = self.blob
+
+    # ------------------------------------------------------------------ device
+    def _device_x(self, X):
+        if isinstance(X, np.ndarray):
+            X = torch.from_numpy(np.ascontiguousarray(X, dtype=self.np_dtype))
+        if X.dtype != self.torch_dtype:
+            X = X.to(self.torch_dtype)
+        if X.device != self.device:
+            X = X.pin_memory().to(self.device, non_blocking=True) if X.device.type == "cpu" else X.to(self.device)
+        if X.dim() != 2 or X.stride(1) != 1:
+            X = X.contiguous()
+        return X
+
+    def shap_device(self, X: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """phi [n_rows][G][M+1] on the device (X already on the device)."""
+        n = X.shape[0]
+        if out is None:
+            out = torch.empty((n, self.n_groups, self.n_features + 1), dtype=self.torch_dtype, device=self.device)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        gts.gts_shap(self.blob.info, self.blob.ptr, X.data_ptr(), n, X.stride(0), out.data_ptr(), st.cuda_stream)
+        return out
+
+    def interactions_device(self, X: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """phi_ij [n_rows][G][M+1][M+1] on the device."""
+        n = X.shape[0]
+        M1 = self.n_features + 1
+        if out is None:
+            out = torch.empty((n, self.n_groups, M1, M1), dtype=self.torch_dtype, device=self.device)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        gts.gts_shap_interactions(self.blob_int.info, self.blob_int.ptr, X.data_ptr(), n, X.stride(0),
+                                  out.data_ptr(), st.cuda_stream)
+        return out
+
+    # ------------------------------------------------------------------- host
+    def shap(self, X) -> np.ndarray:
+        """End to end from host X: H2D, kernels, D2H of phi."""
+        Xd = self._device_x(X)
+        return self.shap_device(Xd).cpu().numpy()
+
+    def shap_interactions(self, X) -> np.ndarray:
+        Xd = self._device_x(X)
+        return self.interactions_device(Xd).cpu().numpy()

@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by
+element, on seeded inputs; plus edge cases and invariants.  Needs a B200."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import brute
+from synth.configs import WORKLOADS
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+
+LAYOUTS = ["nodal", "warp_bins"]
+DTYPES = ["f32", "f64"]
+
+
+def _explainer(ens, dtype="f32", layout="nodal", pack="bfd", max_slots=0, interactions=True):
+    import torch
+    from paper_2010_13972_b200 import TreeShapExplainer
+    return TreeShapExplainer(ens, dtype=dtype, pack=pack, layout=layout, device=torch.device("cuda:0"),
+                             max_slots=max_slots, interactions=interactions)
+
+
+def _run(ex, x, inter=False):
+    import torch
+    xd = torch.from_numpy(np.ascontiguousarray(x, dtype=ex.np_dtype)).cuda()
+    out = ex.interactions_device(xd) if inter else ex.shap_device(xd)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+# --------------------------------------------------------------- fixtures
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_spec_fixtures(gpu, layout, dtype):
+    tol = 1e-12 if dtype == "f64" else 2e-6
+    ex = _explainer(synth.stump(), dtype, layout)
+    np.testing.assert_allclose(_run(ex, [[0.2], [0.9], [0.5]])[:, 0], [[0.6, 0.4], [-0.4, 0.4], [-0.4, 0.4]], atol=tol)
+    ex = _explainer(synth.depth2(), dtype, layout)
+    np.testing.assert_allclose(_run(ex, [[0.2, 0.7]])[0, 0], [1.125, 0.175, 0.7], atol=tol)
+    np.testing.assert_allclose(_run(ex, [[0.2, 0.7]], inter=True)[0, 0],
+                               [[1.05, 0.075, 0], [0.075, 0.1, 0], [0, 0, 0.7]], atol=tol)
+    ex = _explainer(synth.single_leaf(0.7), dtype, layout)
+    np.testing.assert_allclose(_run(ex, [[0.3]])[0, 0], [0.0, 0.7], atol=tol)
+    np.testing.assert_allclose(_run(ex, [[0.3]], inter=True)[0, 0], [[0, 0], [0, 0.7]], atol=tol)
+
+
+# ------------------------------------------------------------ config 1 (brute force)
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_config1_vs_bruteforce(gpu, layout, dtype):
+    w = WORKLOADS["depth3-single"]
+    ens = w.ensemble()
+    x = w.x(ens=ens)
+    ex = _explainer(ens, dtype, layout)
+    phi = _run(ex, x)
+    phi_ij = _run(ex, x, inter=True)
+    ref = np.stack([brute.shap_values(ens, x[r].astype(np.float64)) for r in range(len(x))])[:, None]
+    ref_ij = np.stack([brute.interaction_values(ens, x[r].astype(np.float64)) for r in range(len(x))])[:, None]
+    parity.check(phi, ref, dtype, "shap")
+    parity.check(phi_ij, ref_ij, dtype, "interactions")
+    parity.check(phi, oracle.treeshap(ens, x.astype(np.float64)), dtype, "shap vs O5")
+
+
+# ------------------------------------------------------------- configs 2-5
+
+CASES = [
+    # (workload, n rows checked, n trees subset (None = all), interactions rows)
+    ("cal_housing-small", 2000, None, 500),
+    ("cal_housing-med", 600, None, 64),
+    ("adult-large", 24, None, 4),
+    ("fashion_mnist-med", 24, None, 0),
+    ("covtype-large", 16, 400, 2),
+]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_configs_shap(gpu, case, dtype, layout):
+    name, n, trees, _ = case
+    w = WORKLOADS[name]
+    ens = w.ensemble()
+    if trees is not None:
+        ens = ens.subset(range(trees))
+    x = w.x(n, ens=ens)
+    ex = _explainer(ens, dtype, layout, interactions=False)
+    phi = _run(ex, x)
+    ref = oracle.treeshap(ens, x.astype(np.float64))
+    parity.check(phi, ref, dtype, f"{name} shap")
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("case", [c for c in CASES if c[3] > 0], ids=[c[0] for c in CASES if c[3] > 0])
+def test_configs_interactions(gpu, case, dtype, layout):
+    name, _, trees, n = case
+    w = WORKLOADS[name]
+    ens = w.ensemble()
+    if trees is not None:
+        ens = ens.subset(range(trees))
+    x = w.x(n, ens=ens)
+    ex = _explainer(ens, dtype, layout)
+    got = _run(ex, x, inter=True)
+    ref = oracle.interactions(ens, x.astype(np.float64))
+    parity.check(got, ref, dtype, f"{name} interactions")
+
+
+# ------------------------------------------------------------------ edges
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_ragged_rows_and_padded_ld(gpu, layout):
+    import torch
+    w = WORKLOADS["cal_housing-med"]
+    ens = w.ensemble().subset(range(30))
+    ex = _explainer(ens, "f32", layout)
+    for n in (0, 1, 31, 33, 257, 1000):
+        x = w.x(n, ens=ens)
+        xp = np.zeros((n, 13), np.float32)
+        xp[:, :8] = x
+        xd = torch.from_numpy(xp).cuda()[:, :8]  # ld_x = 13 > M
+        phi = ex.shap_device(xd)
+        torch.cuda.synchronize()
+        if n:
+            parity.check(phi.cpu().numpy(), oracle.treeshap(ens, x.astype(np.float64)), "f32", f"n={n}")
+
+
+def _caterpillar(depth, n_features, seed=0):
+    """A chain tree of the given depth on distinct features: merged k = depth."""
+    rng = np.random.default_rng(seed)
+    feats = rng.permutation(n_features)[:depth]
+    nodes = [None]
+    cover, cur = 2.0 ** 40, 0
+    for d in range(depth):
+        left_c = float(np.floor(cover * rng.uniform(0.2, 0.8)))
+        li, ri = len(nodes), len(nodes) + 1
+        nodes += [None, {"leaf_value": float(rng.normal()), "cover": cover - left_c}]
+        nodes[cur] = {"feature": int(feats[d]), "threshold": float(rng.uniform(0.3, 0.7)), "left": li, "right": ri,
+                      "cover": cover}
+        cur, cover = li, left_c
+    nodes[cur] = {"leaf_value": float(rng.normal()), "cover": cover}
+    return nodes
+
+
+def _nodes_of(ens, t):
+    l, r, f, th, c, v = ens.tree(t)
+    return [({"leaf_value": float(v[j]), "cover": float(c[j])} if l[j] < 0 else
+             {"feature": int(f[j]), "threshold": float(th[j]), "left": int(l[j]), "right": int(r[j]),
+              "cover": float(c[j])}) for j in range(len(l))]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_maximum_path_length(gpu, layout, dtype):
+    """k = 31 distinct features on one path (merged length 32 = the warp), plus
+    short paths in the same model: Q = 16 nodes, full bins."""
+    trees = [_caterpillar(31, 40, seed=1), _caterpillar(20, 40, seed=2), _caterpillar(7, 40, seed=3)]
+    ens = synth.ensemble_from_trees(trees, n_features=40)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0.25, 0.75, (64, 40)).astype(np.float32)
+    ex = _explainer(ens, dtype, layout, max_slots=0 if layout == "warp_bins" else 64, interactions=False)
+    parity.check(_run(ex, x), oracle.treeshap(ens, x.astype(np.float64)), dtype, "k=31 shap")
+
+
+def test_path_too_long_rejected(gpu):
+    from paper_2010_13972_b200 import gts
+    ens = synth.ensemble_from_trees([_caterpillar(32, 40, seed=1)], n_features=40)
+    with pytest.raises(gts.GtsError) as e:
+        gts.gts_extract_paths(ens)
+    assert e.value.status == 3
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_multiclass_base_score_single_leaves(gpu, layout):
+    """G > 1, base_score, single-leaf trees (k = 0 paths only feed the bias)."""
+    ens = synth.make_ensemble(30, 11, 6, 25, n_groups=3, zipf_s=1.2, seed=31)
+    trees = [_nodes_of(ens, t) for t in range(ens.n_trees)] + [[{"leaf_value": 0.3, "cover": 5.0}]] * 2
+    merged = synth.ensemble_from_trees(trees, n_features=11, n_groups=3, base_score=-0.75)
+    x = synth.make_x(32, 300, 11)
+    for dtype in DTYPES:
+        ex = _explainer(merged, dtype, layout)
+        parity.check(_run(ex, x), oracle.treeshap(merged, x.astype(np.float64)), dtype, "multiclass shap")
+        parity.check(_run(ex, x[:40], inter=True), oracle.interactions(merged, x[:40].astype(np.float64)), dtype,
+                     "multiclass interactions")
+
+
+@pytest.mark.parametrize("slots", [16, 32, 64])
+def test_slot_widths_and_wide_model_remap(gpu, slots):
+    """Nodal blobs with every slot width; fashion-shaped M = 784 forces
+    per-chunk feature remaps (slot maps) and flushes."""
+    w = WORKLOADS["fashion_mnist-med"]
+    ens = w.ensemble().subset(range(120))
+    x = w.x(200, ens=ens)
+    ex = _explainer(ens, "f32", "nodal", max_slots=slots, interactions=False)
+    assert ex.blob.info.max_slots == slots
+    parity.check(_run(ex, x), oracle.treeshap(ens, x.astype(np.float64)), "f32", f"slots={slots}")
+
+
+@pytest.mark.parametrize("pack", ["ffd", "bfd", "nf", "none"])
+def test_packing_neutrality(gpu, pack):
+    """Scheduling does not change results."""
+    w = WORKLOADS["cal_housing-med"]
+    ens = w.ensemble()
+    x = w.x(300, ens=ens)
+    ex = _explainer(ens, "f64", "warp_bins", pack=pack, interactions=False)
+    parity.check(_run(ex, x), oracle.treeshap(ens, x.astype(np.float64)), "f64", f"pack={pack}")
+
+
+def test_local_accuracy_full_size(gpu):
+    """At the bench size (cal_housing-med, 2^20 rows, bench launch config):
+    sum(phi) + phi_0 = f(x) for every row (fp32: 1e-3 max(1,|f|)) and exact
+    parity on rows sampled across the whole range."""
+    import torch
+    w = WORKLOADS["cal_housing-med"]
+    ens = w.ensemble()
+    n = 1 << 20
+    x = w.x(n, ens=ens)
+    ex = _explainer(ens, "f32", "nodal")
+    xd = torch.from_numpy(x).cuda()
+    phi = ex.shap_device(xd).cpu().numpy()
+    f = oracle.predict(ens, x.astype(np.float64))
+    assert np.all(np.abs(phi.sum(axis=2) - f) <= 1e-3 * np.maximum(1.0, np.abs(f)))
+    rows = np.unique(np.r_[0, n - 1, np.random.default_rng(0).integers(0, n, 200)])
+    parity.check(phi[rows], oracle.treeshap(ens, x[rows].astype(np.float64)), "f32", "sampled full-size shap")
+    sub = rows[:32]
+    phi_ij = ex.interactions_device(xd).cpu().numpy()
+    parity.check(phi_ij[sub], oracle.interactions(ens, x[sub].astype(np.float64)), "f32", "sampled interactions")
+    np.testing.assert_allclose(phi_ij[:, 0, :8, :8].sum(axis=2), phi[:, 0, :8], atol=2e-4)
