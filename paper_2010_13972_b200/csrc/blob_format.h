@@ -60,7 +60,8 @@ struct ChunkRec {              // 64 bytes
 static_assert(sizeof(ChunkRec) == 64, "chunk size");
 
 struct PathRec {               // 24 bytes
-  int32_t k;                   // non-root merged elements (1..31)
+  int32_t k;                   // non-root merged elements (1..31) | run length << 16 (run heads only):
+                               // a run = consecutive paths of a chunk with one feature set
   int32_t q;                   // Gauss nodes: ceil(k/2)
   int32_t elem;                // first element, relative to the chunk's elem_begin
   int32_t table;               // first word of the path's staged table inside the chunk
@@ -76,13 +77,14 @@ struct ElemRec {               // 24 bytes
 };
 static_assert(sizeof(ElemRec) == 24, "elem size");
 
-// Staged nodal table of one path (T words, shared memory), SHAP kernel:
-//   c[Q]            prod_s A_sq            (A = z + (1-z) t_q)
-//   d[Q]            -v w_q / (1 - t_q)     (phi of every o = 0 element)
-//   per element s:  rho[Q] = B_sq / A_sq   (B = z (1 - t_q)),  C[Q] = v w_q (1 - z_s) / A_sq
+// Staged nodal table of one path (T words, shared memory); every row is padded
+// to QP = round_up(Q, 4) words so it loads with 16-byte vector loads.  SHAP kernel:
+//   c[QP]            prod_s A_sq            (A = z + (1-z) t_q)
+//   d[QP]            -v w_q / (1 - t_q)     (phi of every o = 0 element)
+//   per element s:   rho[QP] = B_sq / A_sq  (B = z (1 - t_q)),  C[QP] = v w_q (1 - z_s) / A_sq
 // Interaction kernel:
-//   c[Q], h[Q] = v w_q / 2, per element: rho[Q], alpha[Q] = (1 - z_s) / A_sq
-GTS_HD inline int nodal_path_words(int k, int q) { return 2 * q + 2 * q * k; }
+//   c[QP], h[QP] = v w_q / 2, per element: rho[QP], alpha[QP] = (1 - z_s) / A_sq
+GTS_HD inline int nodal_path_words(int k, int q) { return 2 * ((q + 3) & ~3) * (k + 1); }
 
 // WARP_BINS lane arrays (each [n_bins * 32], in this order after off_elems):
 //   int32 feature   (-1 root lane, -2 empty lane)

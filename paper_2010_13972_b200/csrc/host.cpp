@@ -463,6 +463,7 @@ struct NodalPlan {
 
 static int pick_slots(int32_t requested, int32_t M) {
   if (requested != 0) return requested;
+  if (M <= 8) return 8;
   if (M <= 16) return 16;
   if (M <= 32) return 32;
   if (M <= 64) return 64;
@@ -481,12 +482,35 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
   const int32_t M = tab.n_features;
   const bool identity = M <= S;
   const int64_t L = tab.n_paths();
-  // paths grouped by group, input order within a group
+  // Paths grouped by group.  Within a group: for identity slot maps, ordered by
+  // (Q descending, feature set, index) so that paths sharing a feature set form
+  // long runs; for per-chunk maps (wide models), input (DFS) order, which keeps
+  // the features of consecutive paths local.
+  auto fs_less = [&](int64_t a, int64_t b) {
+    const int qa = tab.len(a) / 2, qb = tab.len(b) / 2;
+    if (qa != qb) return qa > qb;
+    const int la = tab.len(a), lb = tab.len(b);
+    if (la != lb) return la > lb;
+    for (int i = 1; i < la; ++i) {
+      const int32_t fa = tab.feature[tab.path_offset[a] + i], fb = tab.feature[tab.path_offset[b] + i];
+      if (fa != fb) return fa < fb;
+    }
+    return a < b;
+  };
+  auto same_set = [&](int64_t a, int64_t b) {
+    if (tab.len(a) != tab.len(b)) return false;
+    for (int i = 1; i < tab.len(a); ++i)
+      if (tab.feature[tab.path_offset[a] + i] != tab.feature[tab.path_offset[b] + i]) return false;
+    return true;
+  };
   std::vector<int64_t> order;
   order.reserve(L);
-  for (int32_t g = 0; g < tab.n_groups; ++g)
+  for (int32_t g = 0; g < tab.n_groups; ++g) {
+    const size_t first = order.size();
     for (int64_t p = 0; p < L; ++p)
       if (tab.group[p] == g && tab.len(p) > 1) order.push_back(p);
+    if (identity) std::sort(order.begin() + first, order.end(), fs_less);
+  }
   const int64_t max_words = kChunkTableBytes / (int64_t)tsize;
   int32_t map_id = -1;
   std::vector<int32_t> cur_map;  // sorted features of the current chunk (non-identity)
@@ -523,10 +547,8 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
       feats.resize(M);
       for (int32_t f = 0; f < M; ++f) feats[f] = f;
     }
-    // stable order by q descending inside the chunk (template locality)
-    std::stable_sort(members.begin(), members.end(), [&](int64_t a, int64_t b) {
-      return (tab.len(a) / 2) > (tab.len(b) / 2);
-    });
+    // inside the chunk: Q descending (template locality), then feature set (runs)
+    std::sort(members.begin(), members.end(), fs_less);
     if (feats != cur_map || map_id < 0) {
       ++map_id;
       cur_map = feats;
@@ -541,10 +563,16 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
     c.n_elems = (int32_t)nel;
     int32_t table = 0, rel = 0, maxq = 0;
     double ws = 0, wi = 0;
-    for (int64_t p : members) {
+    size_t run_head = 0;
+    for (size_t mi = 0; mi < members.size(); ++mi) {
+      const int64_t p = members[mi];
       const int k = tab.len(p) - 1, q = (k + 1) / 2;
+      if (mi == 0 || !same_set(members[run_head], p)) run_head = mi;
+      const size_t head_index = np.paths.size() - (mi - run_head);
       PathRec pr{};
       pr.k = k;
+      if (run_head == mi) pr.k |= 1 << 16;
+      else np.paths[head_index].k += 1 << 16;
       pr.q = q;
       pr.elem = rel;
       pr.table = table;
@@ -600,8 +628,8 @@ static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, in
   if (dtype != GTS_F32 && dtype != GTS_F64) return fail(GTS_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
   if (layout != GTS_LAYOUT_NODAL && layout != GTS_LAYOUT_WARP_BINS)
     return fail(GTS_ERR_INVALID_ARGUMENT, "bad layout %d", layout);
-  if (max_slots != 0 && max_slots != 16 && max_slots != 32 && max_slots != 64)
-    return fail(GTS_ERR_INVALID_ARGUMENT, "max_slots must be 0, 16, 32 or 64");
+  if (max_slots != 0 && max_slots != 8 && max_slots != 16 && max_slots != 32 && max_slots != 64)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "max_slots must be 0, 8, 16, 32 or 64");
   const PathTable& tab = *b->tab;
   const size_t tsize = dtype == GTS_F32 ? 4 : 8;
   BlobHeader h{};

@@ -73,7 +73,7 @@ class TreeShapExplainer:
         if build_blobs:
             self.blob = Blob.from_bins(self.bins, self.dtype_code, self.layout, max_slots, self.device)
             if interactions:
-                if self.layout == gts.GTS_LAYOUT_NODAL and self.blob.info.max_slots != 16:
+                if self.layout == gts.GTS_LAYOUT_NODAL and self.blob.info.max_slots > 16:
                     self.blob_int = Blob.from_bins(self.bins, self.dtype_code, self.layout, 16, self.device)
                 else:
                     self.blob_int = self.blob
