@@ -75,12 +75,15 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
   T* const sT = reinterpret_cast<T*>(g_smem);
   const int words = 2 * QP * (k + 1);
   int slot[KM];
-  T acc[R][KM];
+  T acc[R][KM], xv[R][KM];  // the run's slots and this lane's x values, loaded once per run
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
     slot[s] = (s < KM - 1 || s < k) ? E[s].x : 0;
 #pragma unroll
-    for (int r = 0; r < R; ++r) acc[r][s] = (T)0;
+    for (int r = 0; r < R; ++r) {
+      acc[r][s] = (T)0;
+      xv[r][s] = sT[xb[r] + slot[s]];
+    }
   }
   for (int p = 0; p < n_run; ++p) {
     const int4* Ep = E + p * k;
@@ -105,8 +108,8 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
         lds_vec(rho, tp + 2 * QP + s * 2 * QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const bool o = one_fraction(sT[xb[r] + slot[s]], rec);
-          om[r] |= (uint32_t)o << s;
+          const bool o = one_fraction(xv[r][s], rec);
+          if (o) om[r] |= 1u << s;
           if (!o) {
 #pragma unroll
             for (int q = 0; q < Q; ++q) P[r][q] *= rho[q];  // EXTEND: f_s = B_s for o_s = 0
@@ -250,9 +253,13 @@ __device__ __forceinline__ void inter_extend(int k, const int4* __restrict__ E, 
   }
 }
 
-// Small paths (Q <= 3): a run of paths with one feature set, the pair cells of
-// the run accumulated in registers.
-template <typename T, int Q, int R>
+// A run of paths with one feature set (k in {2Q-1, 2Q}, fully unrolled).  Per
+// path and row: P by EXTEND, u_s = (o_s - z_s)/f_s at every node (cached in
+// registers), phi_ij = sum_q W_q u_iq u_jq for i < j, and the diagonal by
+// Eq. 6 from row sums: phi_ii = phi_i - sum_{j != i} phi_ij with
+// phi_i = 2 sum_q W_q u_iq.  kRegAcc: the run's cells accumulate in registers
+// and reach the shared tile once per run (small Q); otherwise per path.
+template <typename T, int Q, int R, bool kRegAcc>
 __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restrict__ E, const T* __restrict__ tab,
                                           const T* __restrict__ gam, const int (&xb)[R], const int (&ab)[R]) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q, NC = KM * (KM + 1) / 2;
@@ -260,37 +267,78 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
   const int words = 2 * QP * (k + 1);
   T G[Q];
   lds_vec(G, gam);
-  T acc[R][NC];
+  int slot[KM], rb[KM];
+  T xv[R][KM];
+#pragma unroll
+  for (int s = 0; s < KM; ++s) {
+    const bool valid = (s < KM - 1 || s < k);
+    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
+    slot[s] = e.x;
+    rb[s] = e.w;
+#pragma unroll
+    for (int r = 0; r < R; ++r) xv[r][s] = sT[xb[r] + e.x];
+  }
+  T acc[R][kRegAcc ? NC : 1];
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc[r][c] = (T)0;
+    for (int c = 0; c < (kRegAcc ? NC : 1); ++c) acc[r][c] = (T)0;
+  auto add = [&](int r, int c, int i, int j, T v) {
+    if constexpr (kRegAcc) acc[r][c] += v;
+    else sT[ab[r] + rb[i] + slot[j]] += v;
+  };
   for (int p = 0; p < n_run; ++p) {
     const int4* Ep = E + p * k;
     const T* tp = tab + p * words;
     T P[R][Q];
     uint32_t om[R];
-    inter_extend<T, Q, R, true>(k, Ep, tp, xb, P, om);
-    T W[R][Q], S2[R][Q];
+    {
+      T c0[Q];
+      lds_vec(c0, tp);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        om[r] = 0u;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) P[r][q] = c0[q];
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < KM; ++s) {
+      if (s < KM - 1 || s < k) {
+        const int4 rec = Ep[s];
+        T rho[Q];
+        lds_vec(rho, tp + 2 * QP + s * 2 * QP);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const bool o = one_fraction(xv[r][s], rec);
+          if (o) om[r] |= 1u << s;
+          if (!o) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) P[r][q] *= rho[q];  // EXTEND at the nodes
+          }
+        }
+      }
+    }
+    T W[R][Q];
     {
       T h[Q];
       lds_vec(h, tp + QP);
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int q = 0; q < Q; ++q) { W[r][q] = h[q] * P[r][q]; S2[r][q] = (T)2; }
+        for (int q = 0; q < Q; ++q) W[r][q] = h[q] * P[r][q];
     }
-    // S2 = 2 - sum_j u_j
+    T u[R][KM][Q];
 #pragma unroll
-    for (int j = 0; j < KM; ++j) {
-      if (j < KM - 1 || j < k) {
+    for (int s = 0; s < KM; ++s) {
+      if (s < KM - 1 || s < k) {
         T al[Q];
-        lds_vec(al, tp + 2 * QP + j * 2 * QP + QP);
+        lds_vec(al, tp + 2 * QP + s * 2 * QP + QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const bool o = (om[r] >> j) & 1u;
+          const bool o = (om[r] >> s) & 1u;
 #pragma unroll
-          for (int q = 0; q < Q; ++q) S2[r][q] -= o ? al[q] : G[q];
+          for (int q = 0; q < Q; ++q) u[r][s][q] = o ? al[q] : G[q];  // UNWIND(s) folded into u
         }
       }
     }
@@ -298,58 +346,51 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
 #pragma unroll
     for (int i = 0; i < KM; ++i) {
       if (i < KM - 1 || i < k) {
-        T ai[Q];
-        lds_vec(ai, tp + 2 * QP + i * 2 * QP + QP);
-        T y[R][Q], yg[R];
+        T y[R][Q], phi[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const bool oi = (om[r] >> i) & 1u;
-          T diag = (T)0, g = (T)0;
+          T a = (T)0;
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
-            const T u = oi ? ai[q] : G[q];
-            y[r][q] = W[r][q] * u;
-            diag = fma(y[r][q], S2[r][q] + u, diag);
-            g = fma(y[r][q], G[q], g);
+            y[r][q] = W[r][q] * u[r][i][q];
+            a += y[r][q];
           }
-          yg[r] = g;
-          acc[r][c] += diag;
+          phi[r] = a + a;  // phi_i
         }
-        ++c;
+        const int cdiag = c++;
 #pragma unroll
         for (int j = i + 1; j < KM; ++j) {
           if (j < KM - 1 || j < k) {
-            T aj[Q];
-            lds_vec(aj, tp + 2 * QP + j * 2 * QP + QP);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-              T s1 = (T)0;
+              T v = (T)0;
 #pragma unroll
-              for (int q = 0; q < Q; ++q) s1 = fma(y[r][q], aj[q], s1);
-              acc[r][c] += ((om[r] >> j) & 1u) ? s1 : yg[r];
+              for (int q = 0; q < Q; ++q) v = fma(y[r][q], u[r][j][q], v);
+              add(r, c, i, j, v);
             }
           }
           ++c;
         }
+        // the diagonal cell collects phi_i; Eq. 6 subtracts the row sums when
+        // the tile is flushed (linear in the paths, so it holds per tile)
+#pragma unroll
+        for (int r = 0; r < R; ++r) add(r, cdiag, i, i, phi[r]);
       } else {
         c += KM - i;
       }
     }
   }
-  // flush: cell order (i, j >= i) row-major over element positions
-  int c = 0;
+  if constexpr (kRegAcc) {
+    int c = 0;
 #pragma unroll
-  for (int i = 0; i < KM; ++i) {
-    const bool iv = (i < KM - 1 || i < k);
-    const int4 ri = iv ? E[i] : make_int4(0, 0, 0, 0);
+    for (int i = 0; i < KM; ++i) {
 #pragma unroll
-    for (int j = i; j < KM; ++j) {
-      if (iv && (j < KM - 1 || j < k)) {
-        const int cell = ri.w + E[j].x;
+      for (int j = i; j < KM; ++j) {
+        if ((i < KM - 1 || i < k) && (j < KM - 1 || j < k))
 #pragma unroll
-        for (int r = 0; r < R; ++r) sT[ab[r] + cell] += acc[r][c];
+          for (int r = 0; r < R; ++r) sT[ab[r] + rb[i] + slot[j]] += acc[r][c];
+        ++c;
       }
-      ++c;
     }
   }
 }
@@ -365,25 +406,14 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
   T P[R][Q];
   uint32_t om[R];
   inter_extend<T, Q, R, kUnroll>(k, E, tp, xb, P, om);
-  T W[R][Q], S2[R][Q];
+  T W[R][Q];
   {
     T h[Q];
     lds_vec(h, tp + QP);
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int q = 0; q < Q; ++q) { W[r][q] = h[q] * P[r][q]; S2[r][q] = (T)2; }
-  }
-#pragma unroll 1
-  for (int j = 0; j < k; ++j) {
-    T al[Q];
-    lds_vec(al, tp + 2 * QP + j * 2 * QP + QP);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const bool o = (om[r] >> j) & 1u;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) S2[r][q] -= o ? al[q] : G[q];
-    }
+      for (int q = 0; q < Q; ++q) W[r][q] = h[q] * P[r][q];
   }
 #pragma unroll 1
   for (int i = 0; i < k; ++i) {
@@ -394,16 +424,16 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool oi = (om[r] >> i) & 1u;
-      T diag = (T)0, g = (T)0;
+      T phi = (T)0, g = (T)0;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         const T u = oi ? ai[q] : G[q];
         y[r][q] = W[r][q] * u;
-        diag = fma(y[r][q], S2[r][q] + u, diag);
+        phi += y[r][q];
         g = fma(y[r][q], G[q], g);
       }
       yg[r] = g;
-      sT[ab[r] + ri.w + ri.x] += diag;
+      sT[ab[r] + ri.w + ri.x] += phi + phi;  // phi_i; Eq. 6 applied at flush
     }
 #pragma unroll 1
     for (int j = i + 1; j < k; ++j) {
@@ -461,26 +491,26 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
   } else {
     const T* gam = gauss + (q - 1) * 3 * kQMax + 2 * kQMax;
     switch (q) {
-#define GTS_IRUN(QQ) case QQ: inter_run<T, QQ, R>(k, n_run, E, tab, gam, xb, ab); break;
-      GTS_IRUN(1) GTS_IRUN(2)
-#undef GTS_IRUN
+      case 1: inter_run<T, 1, R, true>(k, n_run, E, tab, gam, xb, ab); break;
+      case 2: inter_run<T, 2, R, true>(k, n_run, E, tab, gam, xb, ab); break;
       default:
 #pragma unroll 1
         for (int r = 0; r < R; ++r) {
           const int xb1[1] = {xb[r]}, ab1[1] = {ab[r]};
-          if (q == 3) {
-            inter_run<T, 3, 1>(k, n_run, E, tab, gam, xb1, ab1);
-            continue;
-          }
-          for (int p = 0; p < n_run; ++p) {
-            switch (q) {
-#define GTS_IP(QQ, U) case QQ: inter_path<T, QQ, 1, U>(k, E + p * k, tab + p * words, gam, xb1, ab1); break;
-              GTS_IP(4, true) GTS_IP(5, true) GTS_IP(6, false) GTS_IP(7, false) GTS_IP(8, false)
-              GTS_IP(9, false) GTS_IP(10, false) GTS_IP(11, false) GTS_IP(12, false) GTS_IP(13, false)
-              GTS_IP(14, false) GTS_IP(15, false) GTS_IP(16, false)
+          switch (q) {
+            case 3: inter_run<T, 3, 1, true>(k, n_run, E, tab, gam, xb1, ab1); break;
+            case 4: inter_run<T, 4, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break;
+            case 5: inter_run<T, 5, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break;
+            default:
+              for (int p = 0; p < n_run; ++p) {
+                switch (q) {
+#define GTS_IP(QQ) case QQ: inter_path<T, QQ, 1, false>(k, E + p * k, tab + p * words, gam, xb1, ab1); break;
+                  GTS_IP(6) GTS_IP(7) GTS_IP(8) GTS_IP(9) GTS_IP(10) GTS_IP(11) GTS_IP(12) GTS_IP(13)
+                  GTS_IP(14) GTS_IP(15) GTS_IP(16)
 #undef GTS_IP
-              default: break;
-            }
+                  default: break;
+                }
+              }
           }
         }
     }
@@ -635,14 +665,24 @@ __global__ void __launch_bounds__(W * 32, (sizeof(T) == 4 && !kInter) ? 2 : 1) n
         if constexpr (kInter) {
           T* base = out + ((size_t)row[r] * a.G + cur_group) * (size_t)M1 * M1;
           for (int i = 0; i < cur_slots; ++i) {
+            // the diagonal cell holds sum phi_i; Eq. 6: phi_ii = phi_i - sum_{j != i} phi_ij
+            T rowsum = (T)0;
+            for (int j = 0; j < cur_slots; ++j)
+              if (j != i) rowsum += sT[ab[r] + (j < i ? tri_row_base(j, S) + i : tri_row_base(i, S) + j)];
+            const int fi = slotmap[cur_map_begin + i];
+            const T d = sT[ab[r] + tri_row_base(i, S) + i] - rowsum;
+            if (d != (T)0) atomicAdd(base + (size_t)fi * M1 + fi, d);
+          }
+          for (int i = 0; i < cur_slots; ++i) {
             const int fi = slotmap[cur_map_begin + i];
             const int rb = tri_row_base(i, S);
-            for (int j = i; j < cur_slots; ++j) {
+            sT[ab[r] + rb + i] = (T)0;
+            for (int j = i + 1; j < cur_slots; ++j) {
               const T v = sT[ab[r] + rb + j];
               if (v != (T)0) {
                 const int fj = slotmap[cur_map_begin + j];
                 atomicAdd(base + (size_t)fi * M1 + fj, v);
-                if (j != i) atomicAdd(base + (size_t)fj * M1 + fi, v);
+                atomicAdd(base + (size_t)fj * M1 + fi, v);
                 sT[ab[r] + rb + j] = (T)0;
               }
             }
