@@ -1,0 +1,136 @@
+"""The C ABI library (no GPU needed): loads, exports every declared symbol, and
+rejects bad arguments / models with the documented status codes."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import synth
+from paper_2010_13972_b200 import gts
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gts.h")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2010_13972_b200 import _build
+    _build.build()
+    gts.load()
+
+
+def declared_functions():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z0-9_]+\*?\s+\*?(gts_[a-z0-9_]+)\s*\(", txt, flags=re.M)))
+
+
+def test_exports_every_declared_symbol():
+    names = declared_functions()
+    assert len(names) >= 14
+    assert sorted(names) == sorted(gts.EXPORTS)
+    lib = ctypes.CDLL(gts.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    dyn = subprocess.run(["nm", "-D", "--defined-only", gts.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (gts_[a-z0-9_]+)$", dyn, flags=re.M))
+    assert set(names) <= exported
+    assert all(not n.startswith("gts") for n in (set(re.findall(r" T ([A-Za-z0-9_]+)$", dyn, flags=re.M)) - exported)
+               if n.startswith("gts_"))
+
+
+def test_version_and_status_strings():
+    lib = gts.load()
+    assert lib.gts_abi_version() == 1
+    for code, name in gts.STATUS_NAMES.items():
+        assert lib.gts_status_string(code).decode() == name
+
+
+def _status(fn, *a):
+    with pytest.raises(gts.GtsError) as e:
+        fn(*a)
+    return e.value.status
+
+
+def _mut(ens, **kw):
+    e = synth.Ensemble(ens.node_offset.copy(), ens.left.copy(), ens.right.copy(), ens.feature.copy(),
+                       ens.threshold.copy(), ens.cover.copy(), ens.leaf_value.copy(), ens.tree_group.copy(),
+                       ens.n_features, ens.n_groups, ens.base_score)
+    for k, v in kw.items():
+        setattr(e, k, v)
+    return e
+
+
+def test_invalid_models_rejected():
+    base = synth.depth2()
+    bad_cover = base.cover.copy(); bad_cover[3] = 2.0  # 2 + 3 != 4
+    assert _status(gts.gts_extract_paths, _mut(base, cover=bad_cover)) == 2
+    zero_cover = base.cover.copy(); zero_cover[2] = 0.0
+    assert _status(gts.gts_extract_paths, _mut(base, cover=zero_cover)) == 2
+    dangling = base.left.copy(); dangling[1] = 9
+    assert _status(gts.gts_extract_paths, _mut(base, left=dangling)) == 2
+    cyc = base.right.copy(); cyc[1] = 1  # child points to itself
+    assert _status(gts.gts_extract_paths, _mut(base, right=cyc)) == 2
+    feat = base.feature.copy(); feat[0] = 7
+    assert _status(gts.gts_extract_paths, _mut(base, feature=feat)) == 2
+    thr = base.threshold.copy(); thr[0] = np.nan
+    assert _status(gts.gts_extract_paths, _mut(base, threshold=thr)) == 2
+    grp = base.tree_group.copy(); grp[0] = 3
+    assert _status(gts.gts_extract_paths, _mut(base, tree_group=grp)) == 2
+    assert _status(gts.gts_extract_paths, _mut(base, n_features=0)) == 1
+
+
+def test_path_too_long_and_capacity():
+    # a chain of 32 distinct features: merged length 33 > 32 (reading G8)
+    nodes, cover, cur = [None], float(2 ** 40), 0
+    for d in range(32):
+        left_c = float(np.floor(cover / 2))
+        li = len(nodes)
+        nodes += [None, {"leaf_value": 0.1, "cover": cover - left_c}]
+        nodes[cur] = {"feature": d, "threshold": 0.5, "left": li, "right": li + 1, "cover": cover}
+        cur, cover = li, left_c
+    nodes[cur] = {"leaf_value": 0.2, "cover": cover}
+    assert _status(gts.gts_extract_paths, synth.ensemble_from_trees([nodes], n_features=40)) == 3
+    p = gts.gts_extract_paths(synth.depth2())
+    assert _status(gts.gts_binpack, p, 0, "bfd") == 1
+    assert _status(gts.gts_binpack, p, 33, "bfd") == 1
+    assert _status(gts.gts_binpack, p, 2, "bfd") == 3  # a path of length 3 > capacity 2
+    assert _status(gts.gts_binpack, p, 32, 7) == 1
+
+
+def test_blob_plan_and_call_argument_errors():
+    b = gts.gts_binpack(gts.gts_extract_paths(synth.depth2()), 32, "bfd")
+    assert _status(gts.gts_blob_plan, b, 5, 0, 0) == 1
+    assert _status(gts.gts_blob_plan, b, 0, 9, 0) == 1
+    assert _status(gts.gts_blob_plan, b, 0, 0, 12) == 1
+    info = gts.gts_blob_plan(b, gts.GTS_F32, "nodal")
+    assert info.magic == 0x47545342 and info.abi_version == 1 and info.bytes % 256 == 0
+    with pytest.raises(ValueError):
+        gts.gts_blob_write(b, info, np.empty(16, np.uint8))
+    # n_rows == 0 is a no-op; argument errors are caught before any CUDA call
+    gts.gts_shap(info, 0, 0, 0, 2, 0)
+    assert _status(gts.gts_shap, info, 16, 16, -1, 2, 16) == 1
+    assert _status(gts.gts_shap, info, 16, 16, 4, 1, 16) == 1   # ld_x < n_features
+    assert _status(gts.gts_shap, info, 0, 16, 4, 2, 16) == 1    # NULL blob
+    assert _status(gts.gts_shap, info, 8, 16, 4, 2, 16) == 1    # misaligned blob
+    bad = gts.gts_blob_info.from_bytes(info.to_bytes())
+    bad.magic = 0
+    assert _status(gts.gts_shap_interactions, bad, 16, 16, 4, 2, 16) == 1
+
+
+def test_launch_count_and_info_roundtrip():
+    b = gts.gts_binpack(gts.gts_extract_paths(synth.depth2()), 32, "bfd")
+    info = gts.gts_blob_plan(b, gts.GTS_F64, "warp_bins")
+    assert gts.gts_launches_per_call(info, False) == 2
+    again = gts.gts_blob_info.from_bytes(info.to_bytes())
+    assert again.as_dict() == info.as_dict()
+
+
+def test_product_path_fails_loudly_without_library(tmp_path):
+    code = ("import sys; sys.path.insert(0, %r); from paper_2010_13972_b200 import gts; "
+            "gts.load(%r)" % (ROOT, str(tmp_path / "missing.so")))
+    r = subprocess.run(["python", "-c", code], capture_output=True, text=True)
+    assert r.returncode != 0 and "native library missing" in r.stderr
