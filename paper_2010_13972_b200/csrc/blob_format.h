@@ -18,7 +18,7 @@ constexpr uint32_t kMagic = 0x47545342u;  // 'GTSB'
 constexpr int kWarp = 32;                 // bin capacity B = warp size
 constexpr int kQMax = 16;                 // Gauss nodes for merged k <= 31 (k = 2Q max)
 constexpr int kMaxChunkPaths = 256;
-constexpr int kChunkTableBytes = 32 * 1024;  // staged nodal tables per chunk (T words * sizeof(T))
+constexpr int kChunkTableBytes = 16 * 1024;  // staged nodal tables per chunk (T words * sizeof(T))
 
 struct BlobHeader {            // 256 bytes at offset 0
   uint32_t magic, version;

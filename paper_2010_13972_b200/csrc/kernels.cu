@@ -105,22 +105,10 @@ gts_status launch_init(bool inter, const gts_blob_info* info, const char* d_blob
   return cuda_check("init kernel launch");
 }
 
-// Rows per lane: 2 in fp32 (ILP + shared table loads), 1 in fp64.
-template <typename T>
-constexpr int nodal_rows_per_lane() { return sizeof(T) == 4 ? 2 : 1; }
-
-// Warps per block: as many as keep the per-warp tiles within ~150 KB.
-template <typename T, bool kInter, int S>
-constexpr int nodal_warps() {
-  constexpr int R = nodal_rows_per_lane<T>();
-  constexpr size_t per_warp = sizeof(T) * nodal::tile_words_per_warp<T, S, R, kInter>();
-  return per_warp * 8 <= 150 * 1024 ? 8 : (per_warp * 4 <= 150 * 1024 ? 4 : 2);
-}
-
 template <typename T, bool kInter, int S>
 size_t nodal_smem_bytes(const gts_blob_info* info) {
-  constexpr int W = nodal_warps<T, kInter, S>();
-  constexpr int R = nodal_rows_per_lane<T>();
+  constexpr int W = nodal::Cfg<T, kInter, S>::W;
+  constexpr int R = nodal::Cfg<T, kInter, S>::R;
   size_t b = sizeof(T) * ((size_t)nodal::table_word_offset<T, S, W, R, kInter>() + (size_t)info->max_chunk_words);
   b += sizeof(int4) * (size_t)info->max_chunk_elems;
   b += sizeof(int4) * (size_t)info->max_chunk_paths;
@@ -130,8 +118,8 @@ size_t nodal_smem_bytes(const gts_blob_info* info) {
 template <typename T, bool kInter, int S>
 gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const void* d_X, int64_t n_rows, int64_t ld_x,
                         void* out, cudaStream_t st) {
-  constexpr int W = nodal_warps<T, kInter, S>();
-  constexpr int R = nodal_rows_per_lane<T>();
+  constexpr int W = nodal::Cfg<T, kInter, S>::W;
+  constexpr int R = nodal::Cfg<T, kInter, S>::R;
   auto kern = nodal::nodal_kernel<T, S, W, R, kInter>;
   const size_t smem = nodal_smem_bytes<T, kInter, S>(info);
   if (smem > 227 * 1024) return fail(GTS_ERR_INVALID_ARGUMENT, "chunk staging needs %zu bytes of shared memory", smem);

@@ -501,6 +501,14 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
             case 3: inter_run<T, 3, 1, true>(k, n_run, E, tab, gam, xb1, ab1); break;
             case 4: inter_run<T, 4, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break;
             case 5: inter_run<T, 5, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break;
+            case 6:
+              if constexpr (sizeof(T) == 4) { inter_run<T, 6, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break; }
+              [[fallthrough]];
+            case 7:
+              if constexpr (sizeof(T) == 4) {
+                if (q == 7) { inter_run<T, 7, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break; }
+              }
+              [[fallthrough]];
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
@@ -537,6 +545,16 @@ template <typename T, int S, int R, bool kInter>
 __host__ __device__ constexpr int tile_words_per_warp() {
   return R * 32 * ((S + 1) + (acc_width<kInter>(S) | 1));
 }
+
+// Launch shape per (dtype, kernel, slot width): R rows per lane and W warps
+// per block, chosen so that two blocks (tiles + chunk staging) share an SM.
+template <typename T, bool kInter, int S>
+struct Cfg {
+  static constexpr int R = (sizeof(T) == 4 && (kInter ? S <= 8 : S <= 16)) ? 2 : 1;
+  static constexpr int tile_bytes = (int)sizeof(T) * tile_words_per_warp<T, S, R, kInter>();
+  static constexpr int W = tile_bytes * 8 <= 74 * 1024 ? 8 : (tile_bytes * 4 <= 80 * 1024 ? 4 : 2);
+  static constexpr int kMinBlocks = 2;
+};
 
 // shared-memory layout (T words unless noted): gauss | X tiles | phi tiles | table | elems (int4) | paths (int4)
 template <typename T, int S, int W, int R, bool kInter>
@@ -596,7 +614,7 @@ __device__ __forceinline__ void stage_chunk(const ChunkRec& c, const PathRec* __
 }
 
 template <typename T, int S, int W, int R, bool kInter>
-__global__ void __launch_bounds__(W * 32, (sizeof(T) == 4 && !kInter) ? 2 : 1) nodal_kernel(Args a) {
+__global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a) {
   constexpr int XS = S + 1;
   constexpr int AW = acc_width<kInter>(S);
   constexpr int AS = AW | 1;
