@@ -175,7 +175,7 @@ typedef struct gts_blob_info {
   double inter_flops_per_row;
   double paper_shap_flops_per_row;   /* SURVEY.md §8(d) F_shap, for context */
   double paper_inter_flops_per_row;  /* SURVEY.md §8(d) F_int */
-  int64_t max_chunk_words;      /* NODAL: shared-memory staging needs of the largest chunk */
+  int64_t max_chunk_bytes;      /* NODAL: staged bytes of the largest chunk (shared memory) */
   int64_t max_chunk_elems;
   int64_t max_chunk_paths;
   int64_t reserved[5];

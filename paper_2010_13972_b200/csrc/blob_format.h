@@ -18,7 +18,7 @@ constexpr uint32_t kMagic = 0x47545342u;  // 'GTSB'
 constexpr int kWarp = 32;                 // bin capacity B = warp size
 constexpr int kQMax = 16;                 // Gauss nodes for merged k <= 31 (k = 2Q max)
 constexpr int kMaxChunkPaths = 256;
-constexpr int kChunkTableBytes = 16 * 1024;  // staged nodal tables per chunk (T words * sizeof(T))
+constexpr int kChunkBytes = 16 * 1024;    // NODAL: staged bytes per chunk (one TMA bulk copy)
 
 struct BlobHeader {            // 256 bytes at offset 0
   uint32_t magic, version;
@@ -30,11 +30,11 @@ struct BlobHeader {            // 256 bytes at offset 0
   int64_t off_units;           // NODAL: ChunkRec[n_units]; WARP_BINS: int32 kmax[n_units]
   int64_t off_work;            // NODAL: double[2][n_units+1] prefix work (shap, interactions)
   int64_t off_slotmap;         // NODAL: int32 slot -> feature
-  int64_t off_paths;           // NODAL: PathRec[n_kept_paths]
-  int64_t off_elems;           // NODAL: ElemRec[n_kept_elems]; WARP_BINS: lane arrays
+  int64_t off_paths;           // NODAL: start of the staged chunk regions (= off_elems)
+  int64_t off_elems;           // NODAL: staged chunk regions; WARP_BINS: lane arrays
   int64_t n_kept_paths;        // NODAL: paths with k >= 1 (k = 0 paths only feed the bias)
   int64_t n_kept_elems;        // NODAL: non-root elements of the kept paths
-  int64_t max_chunk_words;     // NODAL: largest staged table (T words) of any chunk
+  int64_t max_chunk_bytes;     // NODAL: largest staged region of any chunk
   int64_t max_chunk_elems;     // NODAL: largest element count of any chunk
   int64_t max_chunk_paths;
   int64_t reserved[12];
@@ -42,49 +42,56 @@ struct BlobHeader {            // 256 bytes at offset 0
 static_assert(sizeof(BlobHeader) == 256, "header size");
 
 // NODAL: a chunk = consecutive paths of one group that touch at most max_slots
-// distinct features; a warp walks all of a chunk's paths for its 32 rows.
+// distinct features; a warp walks all of a chunk's paths for its rows.  Its
+// staged region (copied to shared memory with one TMA bulk copy) is
+//   int4 elem[n_elems]  {slot, lower bits, upper bits, tri-row base of slot}
+//   int4 path[n_paths]  {k | run length << 16, Q, first elem, first table word}
+//   T    table[table_words]   (per path, see below)
 struct ChunkRec {              // 64 bytes
   int32_t group;
   int32_t n_paths;
   int32_t n_slots;             // features used by the chunk's slot map
   int32_t map_id;              // equal ids <=> identical slot maps
-  int64_t path_begin;          // index into PathRec[]
-  int64_t elem_begin;          // index into ElemRec[]
+  int64_t path_begin;          // global index of the chunk's first path (bookkeeping)
+  int64_t elem_begin;          // global index of the chunk's first element (bookkeeping)
   int64_t slotmap_begin;       // index into the int32 slot map
   int32_t n_elems;
-  int32_t table_words;         // staged nodal tables (T words)
+  int32_t table_words;         // T words of tables
   int32_t max_q;
-  int32_t pad0;
-  int64_t pad1;
+  int32_t data_bytes;          // staged region size (multiple of 16)
+  int64_t data_off;            // staged region offset in the blob (16-byte aligned)
 };
 static_assert(sizeof(ChunkRec) == 64, "chunk size");
 
-struct PathRec {               // 24 bytes
+// host-side planning records (not stored in the blob)
+struct PathRec {
   int32_t k;                   // non-root merged elements (1..31) | run length << 16 (run heads only):
                                // a run = consecutive paths of a chunk with one feature set
   int32_t q;                   // Gauss nodes: ceil(k/2)
-  int32_t elem;                // first element, relative to the chunk's elem_begin
-  int32_t table;               // first word of the path's staged table inside the chunk
+  int32_t elem;                // first element, relative to the chunk
+  int32_t table;               // first word of the path's table, relative to the chunk's tables
   double v;                    // leaf value
 };
-static_assert(sizeof(PathRec) == 24, "path size");
 
-struct ElemRec {               // 24 bytes
+struct ElemRec {
   int32_t slot;                // feature slot within the chunk's slot map
   float lo, hi;                // lo <= x < hi  <=> o = 1
   int32_t pad;
   double z;                    // merged zero fraction
 };
-static_assert(sizeof(ElemRec) == 24, "elem size");
 
-// Staged nodal table of one path (T words, shared memory); every row is padded
-// to QP = round_up(Q, 4) words so it loads with 16-byte vector loads.  SHAP kernel:
-//   c[QP]            prod_s A_sq            (A = z + (1-z) t_q)
-//   d[QP]            -v w_q / (1 - t_q)     (phi of every o = 0 element)
-//   per element s:   rho[QP] = B_sq / A_sq  (B = z (1 - t_q)),  C[QP] = v w_q (1 - z_s) / A_sq
-// Interaction kernel:
-//   c[QP], h[QP] = v w_q / 2, per element: rho[QP], alpha[QP] = (1 - z_s) / A_sq
-GTS_HD inline int nodal_path_words(int k, int q) { return 2 * ((q + 3) & ~3) * (k + 1); }
+// Nodal table of one path (T words, shared memory).  Every row is padded to
+// QP = round_up(Q, 4) words (16-byte vector loads).  With A_sq = z_s + (1-z_s) t_q,
+// B_sq = z_s (1 - t_q) (f_s(t_q) for o_s = 1 / 0):
+//   c[QP]  prod_s A_sq                  (P(t_q) when every o = 1)
+//   d[QP]  -v w_q / (1 - t_q)           (SHAP: phi of every o = 0 element, times P_q)
+//   h[QP]  v w_q / 2                    (interactions: W_q = h_q P_q)
+//   per element s:
+//     rho[QP]   = B_sq / A_sq           (EXTEND of an o = 0 element)
+//     C[QP]     = v w_q (1 - z_s)/A_sq  (SHAP: phi_s = sum_q P_q C_sq when o_s = 1)
+//     alpha[QP] = (1 - z_s) / A_sq      (interactions: u_sq when o_s = 1)
+GTS_HD constexpr int nodal_qp(int q) { return (q + 3) & ~3; }
+GTS_HD constexpr int nodal_path_words(int k, int q) { return 3 * nodal_qp(q) * (k + 1); }
 
 // WARP_BINS lane arrays (each [n_bins * 32], in this order after off_elems):
 //   int32 feature   (-1 root lane, -2 empty lane)

@@ -512,7 +512,8 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
       if (tab.group[p] == g && tab.len(p) > 1) order.push_back(p);
     if (identity) std::sort(order.begin() + first, order.end(), fs_less);
   }
-  const int64_t max_words = kChunkTableBytes / (int64_t)tsize;
+  // staged bytes of a chunk: element records + path headers (16 B each) + tables
+  auto path_bytes = [&](int k, int q) { return (int64_t)16 * (k + 1) + (int64_t)tsize * nodal_path_words(k, q); };
   int32_t map_id = -1;
   std::vector<int32_t> cur_map;  // sorted features of the current chunk (non-identity)
   size_t i = 0;
@@ -523,14 +524,14 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
     c.elem_begin = (int64_t)np.elems.size();
     std::vector<int32_t> feats;
     std::vector<int64_t> members;
-    int64_t words = 0, nel = 0;
+    int64_t bytes = 0, nel = 0;
     size_t j = i;
     while (j < order.size() && (int)members.size() < kMaxChunkPaths) {
       const int64_t p = order[j];
       if (tab.group[p] != c.group) break;
       const int k = tab.len(p) - 1, q = (k + 1) / 2;
-      const int64_t w = nodal_path_words(k, q);
-      if (!members.empty() && words + w > max_words) break;
+      const int64_t w = path_bytes(k, q);
+      if (!members.empty() && bytes + w > kChunkBytes) break;
       if (!identity) {
         std::vector<int32_t> u = feats;
         for (int64_t e = tab.path_offset[p] + 1; e < tab.path_offset[p + 1]; ++e) u.push_back(tab.feature[e]);
@@ -540,7 +541,7 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
         feats.swap(u);
       }
       members.push_back(p);
-      words += w;
+      bytes += w;
       nel += k;
       ++j;
     }
@@ -596,7 +597,9 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
     }
     c.table_words = table;
     c.max_q = maxq;
-    np.max_words = std::max<int64_t>(np.max_words, table);
+    c.data_bytes = (int32_t)(16 * ((int64_t)nel + c.n_paths) + (int64_t)tsize * table);
+    c.data_bytes = (c.data_bytes + 15) & ~15;
+    np.max_words = std::max<int64_t>(np.max_words, c.data_bytes);
     np.max_elems = std::max<int64_t>(np.max_elems, nel);
     np.max_paths = std::max<int64_t>(np.max_paths, c.n_paths);
     np.chunks.push_back(c);
@@ -671,7 +674,7 @@ static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, in
     h.n_units = (int64_t)P.chunks.size();
     h.n_kept_paths = (int64_t)P.paths.size();
     h.n_kept_elems = (int64_t)P.elems.size();
-    h.max_chunk_words = P.max_words;
+    h.max_chunk_bytes = P.max_words;
     h.max_chunk_elems = P.max_elems;
     h.max_chunk_paths = P.max_paths;
     h.off_gauss = off;
@@ -682,10 +685,12 @@ static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, in
     off = align256(off + 8 * 2 * (h.n_units + 1));
     h.off_slotmap = off;
     off = align256(off + 4 * (int64_t)P.slotmap.size());
-    h.off_paths = off;
-    off = align256(off + (int64_t)sizeof(PathRec) * h.n_kept_paths);
-    h.off_elems = off;
-    off = align256(off + (int64_t)sizeof(ElemRec) * h.n_kept_elems);
+    h.off_paths = h.off_elems = off;  // staged chunk regions, back to back
+    for (ChunkRec& c : P.chunks) {
+      c.data_off = off;
+      off += c.data_bytes;
+    }
+    off = align256(off);
   } else {
     h.max_slots = 0;
     h.n_units = b->n_bins;
@@ -718,7 +723,7 @@ static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, in
   info->inter_flops_per_row = fi;
   info->paper_shap_flops_per_row = ps;
   info->paper_inter_flops_per_row = pi;
-  info->max_chunk_words = h.max_chunk_words;
+  info->max_chunk_bytes = h.max_chunk_bytes;
   info->max_chunk_elems = h.max_chunk_elems;
   info->max_chunk_paths = h.max_chunk_paths;
   if (hdr) *hdr = h;
@@ -736,6 +741,61 @@ static void write_gauss(char* dst) {
       row[q] = q < Q ? (T)t[q] : (T)0;
       row[kQMax + q] = q < Q ? (T)w[q] : (T)0;
       row[2 * kQMax + q] = q < Q ? (T)(-1.0L / (1.0L - t[q])) : (T)0;
+    }
+  }
+}
+
+// Staged chunk regions (blob_format.h): element records, path headers, and the
+// nodal tables, computed in long double from the fp64 zero fractions and leaf
+// values and rounded once to T (reading G11: one rounding in fp32 mode).
+template <typename T>
+static void write_regions(const NodalPlan& np, int S, char* out) {
+  long double tq[kQMax + 1][kQMax], wq[kQMax + 1][kQMax];
+  for (int Q = 1; Q <= kQMax; ++Q) gauss_legendre01(Q, tq[Q], wq[Q]);
+  const int64_t C = (int64_t)np.chunks.size();
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t ci = 0; ci < C; ++ci) {
+    const ChunkRec& c = np.chunks[ci];
+    char* region = out + c.data_off;
+    int32_t* E = reinterpret_cast<int32_t*>(region);
+    int32_t* Pp = E + 4 * (int64_t)c.n_elems;
+    T* tab = reinterpret_cast<T*>(Pp + 4 * (int64_t)c.n_paths);
+    for (int32_t e = 0; e < c.n_elems; ++e) {
+      const ElemRec& er = np.elems[c.elem_begin + e];
+      int32_t lo, hi;
+      std::memcpy(&lo, &er.lo, 4);
+      std::memcpy(&hi, &er.hi, 4);
+      E[4 * e + 0] = er.slot;
+      E[4 * e + 1] = lo;
+      E[4 * e + 2] = hi;
+      E[4 * e + 3] = er.slot * (2 * S - er.slot - 1) / 2;  // upper-triangle row base of the slot
+    }
+    for (int32_t p = 0; p < c.n_paths; ++p) {
+      const PathRec& pr = np.paths[c.path_begin + p];
+      Pp[4 * p + 0] = pr.k;
+      Pp[4 * p + 1] = pr.q;
+      Pp[4 * p + 2] = pr.elem;
+      Pp[4 * p + 3] = pr.table;
+      const int k = pr.k & 0xff, Q = pr.q, QP = nodal_qp(Q);
+      const ElemRec* el = &np.elems[c.elem_begin + pr.elem];
+      T* t = tab + pr.table;
+      const long double v = pr.v;
+      for (int q = 0; q < Q; ++q) {
+        const long double tt = tq[Q][q], w = wq[Q][q];
+        long double cq = 1.0L;
+        for (int s = 0; s < k; ++s) cq *= (long double)el[s].z + (1.0L - el[s].z) * tt;
+        t[q] = (T)cq;
+        t[QP + q] = (T)(-v * w / (1.0L - tt));
+        t[2 * QP + q] = (T)(0.5L * v * w);
+        for (int s = 0; s < k; ++s) {
+          const long double z = el[s].z;
+          const long double A = z + (1.0L - z) * tt, B = z * (1.0L - tt);
+          T* row = t + 3 * QP + s * 3 * QP;
+          row[q] = (T)(B / A);
+          row[QP + q] = (T)(v * w * (1.0L - z) / A);
+          row[2 * QP + q] = (T)((1.0L - z) / A);
+        }
+      }
     }
   }
 }
@@ -811,8 +871,8 @@ static gts_status blob_write(const gts_bins* b, const gts_blob_info* info, void*
       wi[c + 1] = wi[c] + np.work_inter[c];
     }
     std::memcpy(out + h.off_slotmap, np.slotmap.data(), 4 * np.slotmap.size());
-    std::memcpy(out + h.off_paths, np.paths.data(), sizeof(PathRec) * np.paths.size());
-    std::memcpy(out + h.off_elems, np.elems.data(), sizeof(ElemRec) * np.elems.size());
+    if (h.dtype == GTS_F32) write_regions<float>(np, h.max_slots, out);
+    else write_regions<double>(np, h.max_slots, out);
   } else {
     if (h.dtype == GTS_F32) write_bins<float>(*b, bp, h, out);
     else write_bins<double>(*b, bp, h, out);

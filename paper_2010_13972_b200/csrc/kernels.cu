@@ -105,14 +105,16 @@ gts_status launch_init(bool inter, const gts_blob_info* info, const char* d_blob
   return cuda_check("init kernel launch");
 }
 
+size_t nodal_buffer_bytes(const gts_blob_info* info) {
+  return ((size_t)info->max_chunk_bytes + 127) & ~size_t(127);
+}
+
 template <typename T, bool kInter, int S>
 size_t nodal_smem_bytes(const gts_blob_info* info) {
   constexpr int W = nodal::Cfg<T, kInter, S>::W;
   constexpr int R = nodal::Cfg<T, kInter, S>::R;
-  size_t b = sizeof(T) * ((size_t)nodal::table_word_offset<T, S, W, R, kInter>() + (size_t)info->max_chunk_words);
-  b += sizeof(int4) * (size_t)info->max_chunk_elems;
-  b += sizeof(int4) * (size_t)info->max_chunk_paths;
-  return b;
+  // tiles, then two TMA staging buffers (double buffering) and their mbarriers
+  return (size_t)nodal::staging_byte_offset<T, S, W, R, kInter>() + 2 * nodal_buffer_bytes(info) + 16;
 }
 
 template <typename T, bool kInter, int S>
@@ -141,9 +143,7 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   a.M = info->n_features;
   a.G = info->n_groups;
   a.n_chunks = info->n_units;
-  a.max_elems = (int)info->max_chunk_elems;
-  a.max_paths = (int)info->max_chunk_paths;
-  a.max_words = (int)info->max_chunk_words;
+  a.max_chunk_bytes = (int)nodal_buffer_bytes(info);
   if (info->n_units == 0) return GTS_OK;
   const int64_t blocks = row_tiles * splits;
   if (blocks > INT32_MAX) return fail(GTS_ERR_INVALID_ARGUMENT, "too many rows");

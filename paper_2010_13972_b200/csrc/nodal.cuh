@@ -73,7 +73,7 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
                                          const int (&xb)[R], const int (&ab)[R]) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q;
   T* const sT = reinterpret_cast<T*>(g_smem);
-  const int words = 2 * QP * (k + 1);
+  const int words = nodal_path_words(k, Q);
   int slot[KM];
   T acc[R][KM], xv[R][KM];  // the run's slots and this lane's x values, loaded once per run
 #pragma unroll
@@ -105,7 +105,7 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
       if (s < KM - 1 || s < k) {
         const int4 rec = Ep[s];
         T rho[Q];
-        lds_vec(rho, tp + 2 * QP + s * 2 * QP);
+        lds_vec(rho, tp + 3 * QP + s * 3 * QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool o = one_fraction(xv[r][s], rec);
@@ -133,7 +133,7 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
         T C[Q];
-        lds_vec(C, tp + 2 * QP + s * 2 * QP + QP);
+        lds_vec(C, tp + 3 * QP + s * 3 * QP + QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           T a = (T)0;
@@ -173,7 +173,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
   for (int s = 0; s < k; ++s) {
     const int4 rec = E[s];
     T rho[Q];
-    lds_vec(rho, tab + 2 * QP + s * 2 * QP);
+    lds_vec(rho, tab + 3 * QP + s * 3 * QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool o = one_fraction(sT[xb[r] + rec.x], rec);
@@ -200,7 +200,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
   for (int s = 0; s < k; ++s) {
     const int sl = E[s].x;
     T C[Q];
-    lds_vec(C, tab + 2 * QP + s * 2 * QP + QP);
+    lds_vec(C, tab + 3 * QP + s * 3 * QP + QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       T a = (T)0;
@@ -232,7 +232,7 @@ __device__ __forceinline__ void inter_extend(int k, const int4* __restrict__ E, 
   auto body = [&](int s) {
     const int4 rec = E[s];
     T rho[Q];
-    lds_vec(rho, tp + 2 * QP + s * 2 * QP);
+    lds_vec(rho, tp + 3 * QP + s * 3 * QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool o = one_fraction(sT[xb[r] + rec.x], rec);
@@ -264,7 +264,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
                                           const T* __restrict__ gam, const int (&xb)[R], const int (&ab)[R]) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q, NC = KM * (KM + 1) / 2;
   T* const sT = reinterpret_cast<T*>(g_smem);
-  const int words = 2 * QP * (k + 1);
+  const int words = nodal_path_words(k, Q);
   T G[Q];
   lds_vec(G, gam);
   int slot[KM], rb[KM];
@@ -307,7 +307,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
       if (s < KM - 1 || s < k) {
         const int4 rec = Ep[s];
         T rho[Q];
-        lds_vec(rho, tp + 2 * QP + s * 2 * QP);
+        lds_vec(rho, tp + 3 * QP + s * 3 * QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool o = one_fraction(xv[r][s], rec);
@@ -322,7 +322,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
     T W[R][Q];
     {
       T h[Q];
-      lds_vec(h, tp + QP);
+      lds_vec(h, tp + 2 * QP);
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -333,7 +333,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
         T al[Q];
-        lds_vec(al, tp + 2 * QP + s * 2 * QP + QP);
+        lds_vec(al, tp + 3 * QP + s * 3 * QP + 2 * QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool o = (om[r] >> s) & 1u;
@@ -409,7 +409,7 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
   T W[R][Q];
   {
     T h[Q];
-    lds_vec(h, tp + QP);
+    lds_vec(h, tp + 2 * QP);
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -419,7 +419,7 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
   for (int i = 0; i < k; ++i) {
     const int4 ri = E[i];
     T ai[Q];
-    lds_vec(ai, tp + 2 * QP + i * 2 * QP + QP);
+    lds_vec(ai, tp + 3 * QP + i * 3 * QP + 2 * QP);
     T y[R][Q], yg[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -439,7 +439,7 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
     for (int j = i + 1; j < k; ++j) {
       const int cell = ri.w + E[j].x;
       T aj[Q];
-      lds_vec(aj, tp + 2 * QP + j * 2 * QP + QP);
+      lds_vec(aj, tp + 3 * QP + j * 3 * QP + 2 * QP);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         T s1 = (T)0;
@@ -462,7 +462,7 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
   const int k = ph.x & 0xff, n_run = ph.x >> 16, q = ph.y;
   const int4* E = E0 + ph.z;
   const T* tab = table + ph.w;
-  const int words = 2 * ((q + 3) & ~3) * (k + 1);
+  const int words = nodal_path_words(k, q);
   if constexpr (!kInter) {
     switch (q) {
 #define GTS_RUN(QQ) case QQ: shap_run<T, QQ, R>(k, n_run, E, tab, xb, ab); break;
@@ -535,7 +535,7 @@ struct Args {
   int n_splits;
   int M, G;
   int64_t n_chunks;
-  int max_elems, max_paths, max_words;
+  int max_chunk_bytes;
 };
 
 template <bool kInter>
@@ -556,61 +556,40 @@ struct Cfg {
   static constexpr int kMinBlocks = 2;
 };
 
-// shared-memory layout (T words unless noted): gauss | X tiles | phi tiles | table | elems (int4) | paths (int4)
+// shared-memory layout: gauss (T) | X tiles (T) | phi tiles (T) | 2 staging buffers | 2 mbarriers
 template <typename T, int S, int W, int R, bool kInter>
-__host__ __device__ constexpr int table_word_offset() {
-  return ((kQMax * 3 * kQMax + W * tile_words_per_warp<T, S, R, kInter>()) + 3) & ~3;
+__host__ __device__ constexpr int staging_byte_offset() {
+  return (((kQMax * 3 * kQMax + W * tile_words_per_warp<T, S, R, kInter>()) * (int)sizeof(T)) + 127) & ~127;
 }
 
-// Stage chunk c: element records, path headers, nodal tables (computed in fp64
-// from the blob's fp64 zero fractions, rounded once to T).
-template <typename T, bool kInter>
-__device__ __forceinline__ void stage_chunk(const ChunkRec& c, const PathRec* __restrict__ gpaths,
-                                            const ElemRec* __restrict__ gelems, int S, int o_table, int b_elem,
-                                            int b_path, int nwarps) {
-  T* const sT = reinterpret_cast<T*>(g_smem);
-  int4* const sE = reinterpret_cast<int4*>(g_smem + b_elem);
-  int4* const sP = reinterpret_cast<int4*>(g_smem + b_path);
-  const int tid = threadIdx.x, nth = blockDim.x;
-  for (int e = tid; e < c.n_elems; e += nth) {
-    const ElemRec er = gelems[c.elem_begin + e];
-    sE[e] = make_int4(er.slot, __float_as_int(er.lo), __float_as_int(er.hi), tri_row_base(er.slot, S));
-  }
-  for (int p = tid; p < c.n_paths; p += nth) {
-    const PathRec pr = gpaths[c.path_begin + p];
-    sP[p] = make_int4(pr.k, pr.q, pr.elem, pr.table);  // pr.k holds k | run_len << 16
-  }
-  const int warp = tid >> 5, lane = tid & 31;
-  const T* gauss = sT;
-  for (int p = warp; p < c.n_paths; p += nwarps) {
-    const PathRec pr = gpaths[c.path_begin + p];
-    const int k = pr.k & 0xff, Q = pr.q, QP = (Q + 3) & ~3;
-    const ElemRec* el = gelems + c.elem_begin + pr.elem;
-    T* tab = sT + o_table + pr.table;
-    const T* g = gauss + (Q - 1) * 3 * kQMax;
-    for (int idx = lane; idx < k * Q; idx += 32) {
-      const int s = idx / Q, q = idx - s * Q;
-      const double z = el[s].z, t = (double)g[q];
-      const double A = z + (1.0 - z) * t;  // f_s(t_q), o_s = 1
-      const double B = z * (1.0 - t);      // f_s(t_q), o_s = 0
-      T* row = tab + 2 * QP + s * 2 * QP;
-      row[q] = (T)(B / A);                 // rho
-      if (kInter) row[QP + q] = (T)((1.0 - z) / A);                          // alpha
-      else row[QP + q] = (T)(pr.v * (double)g[kQMax + q] * (1.0 - z) / A);   // C
-    }
-    if (lane < Q) {
-      const int q = lane;
-      const double t = (double)g[q], w = (double)g[kQMax + q];
-      double cq = 1.0;
-      for (int s = 0; s < k; ++s) {
-        const double z = el[s].z;
-        cq *= z + (1.0 - z) * t;
-      }
-      tab[q] = (T)cq;
-      if (kInter) tab[QP + q] = (T)(0.5 * pr.v * w);
-      else tab[QP + q] = (T)(-pr.v * w / (1.0 - t));
-    }
-  }
+// ---- TMA bulk copy (global -> shared) completing on an mbarrier (PTX ISA:
+//      cp.async.bulk, mbarrier.*); SASS shows UBLKCP / SYNCS.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
 }
 
 template <typename T, int S, int W, int R, bool kInter>
@@ -621,21 +600,18 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
   constexpr int ROWS = 32 * R;
   constexpr int o_x = kQMax * 3 * kQMax;
   constexpr int o_acc = o_x + W * ROWS * XS;
-  constexpr int o_table = table_word_offset<T, S, W, R, kInter>();
-  const int b_elem = (o_table + a.max_words) * (int)sizeof(T);
-  const int b_path = b_elem + 16 * a.max_elems;
+  constexpr int b_stage = staging_byte_offset<T, S, W, R, kInter>();
+  const int buf_bytes = a.max_chunk_bytes;  // multiple of 128 (host rounding)
+  unsigned char* const stage0 = g_smem + b_stage;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(stage0 + 2 * buf_bytes);
 
   const BlobHeader* hdr = reinterpret_cast<const BlobHeader*>(a.blob);
   const ChunkRec* chunks = reinterpret_cast<const ChunkRec*>(a.blob + hdr->off_units);
   const double* work = reinterpret_cast<const double*>(a.blob + hdr->off_work) + (kInter ? (a.n_chunks + 1) : 0);
   const int32_t* slotmap = reinterpret_cast<const int32_t*>(a.blob + hdr->off_slotmap);
-  const PathRec* gpaths = reinterpret_cast<const PathRec*>(a.blob + hdr->off_paths);
-  const ElemRec* gelems = reinterpret_cast<const ElemRec*>(a.blob + hdr->off_elems);
   const T* X = static_cast<const T*>(a.X);
   T* out = static_cast<T*>(a.out);
   T* const sT = reinterpret_cast<T*>(g_smem);
-  const int4* const sE = reinterpret_cast<const int4*>(g_smem + b_elem);
-  const int4* const sP = reinterpret_cast<const int4*>(g_smem + b_path);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t row_tile = blockIdx.x / a.n_splits;
@@ -655,6 +631,17 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
   };
   const int64_t c_begin = split_begin(split), c_end = split_begin(split + 1);
 
+  // prologue: barriers, first chunk in flight, gauss table, zeroed tiles
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+    if (c_begin < c_end) {
+      const ChunkRec c0 = chunks[c_begin];
+      mbar_expect_tx(&bars[0], (uint32_t)c0.data_bytes);
+      tma_bulk_g2s(stage0, a.blob + c0.data_off, (uint32_t)c0.data_bytes, &bars[0]);
+    }
+  }
   const T* gsrc = reinterpret_cast<const T*>(a.blob + hdr->off_gauss);
   for (int i = tid; i < kQMax * 3 * kQMax; i += blockDim.x) sT[i] = gsrc[i];
   int xb[R], ab[R];
@@ -720,10 +707,16 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
     dirty = false;
   };
 
+  uint32_t phase[2] = {0u, 0u};
   for (int64_t ci = c_begin; ci < c_end; ++ci) {
+    const int b = (int)((ci - c_begin) & 1);
     const ChunkRec c = chunks[ci];
-    __syncthreads();  // previous chunk's tables no longer in use
-    stage_chunk<T, kInter>(c, gpaths, gelems, S, o_table, b_elem, b_path, W);
+    __syncthreads();  // every warp is done with buffer b^1 (chunk ci-1)
+    if (tid == 0 && ci + 1 < c_end) {  // prefetch the next chunk while this one computes
+      const ChunkRec cn = chunks[ci + 1];
+      mbar_expect_tx(&bars[b ^ 1], (uint32_t)cn.data_bytes);
+      tma_bulk_g2s(stage0 + (b ^ 1) * buf_bytes, a.blob + cn.data_off, (uint32_t)cn.data_bytes, &bars[b ^ 1]);
+    }
     if (c.map_id != cur_map || c.group != cur_group) {
       flush();
       if (c.map_id != cur_map) {
@@ -737,11 +730,15 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
       cur_slots = c.n_slots;
       cur_map_begin = c.slotmap_begin;
     }
-    __syncthreads();  // tables staged
+    mbar_wait(&bars[b], phase[b]);
+    phase[b] ^= 1u;
     if (row0 < a.n_rows) {
+      const int4* sE = reinterpret_cast<const int4*>(stage0 + b * buf_bytes);
+      const int4* sP = sE + c.n_elems;
+      const T* tab = reinterpret_cast<const T*>(sP + c.n_paths);
       for (int p = 0; p < c.n_paths;) {
         const int4 ph = sP[p];
-        run_dispatch<T, R, kInter>(ph, sE, sT + o_table, sT, xb, ab);
+        run_dispatch<T, R, kInter>(ph, sE, tab, sT, xb, ab);
         p += ph.x >> 16;
       }
       dirty = true;

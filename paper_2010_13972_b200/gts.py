@@ -57,7 +57,7 @@ class gts_blob_info(ctypes.Structure):
                 ("n_paths", _i64), ("n_elems", _i64), ("n_units", _i64), ("bytes", _i64),
                 ("shap_flops_per_row", _dbl), ("inter_flops_per_row", _dbl),
                 ("paper_shap_flops_per_row", _dbl), ("paper_inter_flops_per_row", _dbl),
-                ("max_chunk_words", _i64), ("max_chunk_elems", _i64), ("max_chunk_paths", _i64),
+                ("max_chunk_bytes", _i64), ("max_chunk_elems", _i64), ("max_chunk_paths", _i64),
                 ("reserved", _i64 * 5)]
 
     def to_bytes(self) -> bytes:
