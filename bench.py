@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
     ap.add_argument("--layout", choices=["nodal", "warp_bins"], default="nodal")
     ap.add_argument("--pack", default="bfd")
+    ap.add_argument("--x-layout", choices=["row", "feature"], default="row",
+                    help="X row-major [n][M] or feature-major (gts_shap_strided, row_stride 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ablation", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -273,8 +275,13 @@ def run_ours(args):
 
     # --- this rank's rows (counter-keyed generator: no scatter)
     x_host = w.x(n, row0=rank * n, ens=ens if w.tie_frac > 0 else None)
-    xt = torch.from_numpy(x_host if args.dtype == "f32" else x_host.astype(np.float64))
+    xh = x_host if args.dtype == "f32" else x_host.astype(np.float64)
+    if args.x_layout == "feature":  # [n][M] view of a feature-major [M][n] buffer
+        xt = torch.from_numpy(np.ascontiguousarray(xh.T)).t()
+    else:
+        xt = torch.from_numpy(xh)
     xd = xt.to(dev)
+    x_rs, x_cs = TreeShapExplainer._strides(xd)
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     phi = torch.empty((n, G, M + 1), dtype=tdt, device=dev) if do_shap else None
     phi_ij = torch.empty((n, G, M + 1, M + 1), dtype=tdt, device=dev) if do_int else None
@@ -284,11 +291,12 @@ def run_ours(args):
     def step(evs=None):
         if do_shap:
             if evs: evs[0].record(stream)
-            gts.gts_shap(info_s, ex.blob.ptr, xd.data_ptr(), n, xd.stride(0), phi.data_ptr(), stream.cuda_stream)
+            gts.gts_shap_strided(info_s, ex.blob.ptr, xd.data_ptr(), n, x_rs, x_cs, phi.data_ptr(),
+                                 stream.cuda_stream)
             if evs: evs[1].record(stream)
         if do_int:
             if evs: evs[2].record(stream)
-            gts.gts_shap_interactions(info_i, ex.blob_int.ptr, xd.data_ptr(), n, xd.stride(0), phi_ij.data_ptr(),
+            gts.gts_shap_interactions_strided(info_i, ex.blob_int.ptr, xd.data_ptr(), n, x_rs, x_cs, phi_ij.data_ptr(),
                                       stream.cuda_stream)
             if evs: evs[3].record(stream)
 
@@ -441,7 +449,7 @@ def run_ours(args):
         "config": {"workload": args.workload, "mode": args.mode, "rows_per_gpu": n, "global_rows": total_rows,
                    "trees": w.n_trees, "max_depth": w.max_depth, "features": M, "groups": G,
                    "paths": int(info_s.n_paths), "path_elems": int(info_s.n_elems), "layout": args.layout,
-                   "pack": args.pack, "bins": int(bins_view["n_bins"]),
+                   "pack": args.pack, "x_layout": args.x_layout, "bins": int(bins_view["n_bins"]),
                    "bin_utilisation": round(float(bins_view["utilisation"]), 6),
                    "l2": "flushed between timed steps (512 MiB memset outside the events); phi_ij > L2",
                    "parallelism": f"dp{world}: rows sharded, path table replicated by one NCCL broadcast"},

@@ -210,6 +210,18 @@ gts_status gts_shap(const gts_blob_info* info, const void* d_blob, const void* d
 gts_status gts_shap_interactions(const gts_blob_info* info, const void* d_blob, const void* d_X,
                                  int64_t n_rows, int64_t ld_x, void* d_phi_ij, void* stream);
 
+/* Same two calls for X in either layout: element (r, f) at
+   d_X[r * row_stride + f * col_stride], with row-major (col_stride == 1,
+   row_stride >= n_features) or feature-major (row_stride == 1,
+   col_stride >= n_rows).  Feature-major X makes the per-chunk gathers of wide
+   models (many features per row) coalesced.  gts_shap(..., ld_x, ...) is
+   gts_shap_strided(..., ld_x, 1, ...). */
+gts_status gts_shap_strided(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
+                            int64_t row_stride, int64_t col_stride, void* d_phi, void* stream);
+gts_status gts_shap_interactions_strided(const gts_blob_info* info, const void* d_blob, const void* d_X,
+                                         int64_t n_rows, int64_t row_stride, int64_t col_stride, void* d_phi_ij,
+                                         void* stream);
+
 /* Number of kernel launches one gts_shap / gts_shap_interactions call issues. */
 int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions);
 

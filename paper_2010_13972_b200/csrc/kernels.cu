@@ -118,8 +118,8 @@ size_t nodal_smem_bytes(const gts_blob_info* info) {
 }
 
 template <typename T, bool kInter, int S>
-gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const void* d_X, int64_t n_rows, int64_t ld_x,
-                        void* out, cudaStream_t st) {
+gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const void* d_X, int64_t n_rows, int64_t rs,
+                        int64_t cs, void* out, cudaStream_t st) {
   constexpr int W = nodal::Cfg<T, kInter, S>::W;
   constexpr int R = nodal::Cfg<T, kInter, S>::R;
   auto kern = nodal::nodal_kernel<T, S, W, R, kInter>;
@@ -137,7 +137,8 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   a.blob = d_blob;
   a.X = d_X;
   a.n_rows = n_rows;
-  a.ld_x = ld_x;
+  a.row_stride = rs;
+  a.col_stride = cs;
   a.out = out;
   a.n_splits = (int)splits;
   a.M = info->n_features;
@@ -153,16 +154,16 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
 
 template <typename T, bool kInter>
 gts_status launch_nodal_s(const gts_blob_info* info, const char* d_blob, const void* d_X, int64_t n_rows,
-                          int64_t ld_x, void* out, cudaStream_t st) {
+                          int64_t rs, int64_t cs, void* out, cudaStream_t st) {
   switch (info->max_slots) {
-    case 8: return launch_nodal<T, kInter, 8>(info, d_blob, d_X, n_rows, ld_x, out, st);
-    case 16: return launch_nodal<T, kInter, 16>(info, d_blob, d_X, n_rows, ld_x, out, st);
+    case 8: return launch_nodal<T, kInter, 8>(info, d_blob, d_X, n_rows, rs, cs, out, st);
+    case 16: return launch_nodal<T, kInter, 16>(info, d_blob, d_X, n_rows, rs, cs, out, st);
     case 32:
       if constexpr (kInter) break;
-      else return launch_nodal<T, kInter, 32>(info, d_blob, d_X, n_rows, ld_x, out, st);
+      else return launch_nodal<T, kInter, 32>(info, d_blob, d_X, n_rows, rs, cs, out, st);
     case 64:
       if constexpr (kInter) break;
-      else return launch_nodal<T, kInter, 64>(info, d_blob, d_X, n_rows, ld_x, out, st);
+      else return launch_nodal<T, kInter, 64>(info, d_blob, d_X, n_rows, rs, cs, out, st);
     default: break;
   }
   return fail(GTS_ERR_INVALID_ARGUMENT,
@@ -172,15 +173,16 @@ gts_status launch_nodal_s(const gts_blob_info* info, const char* d_blob, const v
 }
 
 template <typename T, bool kInter>
-gts_status launch_bins(const gts_blob_info* info, const char* d_blob, const void* d_X, int64_t n_rows, int64_t ld_x,
-                       void* out, cudaStream_t st) {
+gts_status launch_bins(const gts_blob_info* info, const char* d_blob, const void* d_X, int64_t n_rows, int64_t rs,
+                       int64_t cs, void* out, cudaStream_t st) {
   constexpr int W = 4;
   if (info->n_units == 0) return GTS_OK;
   wb::BinArgs a;
   a.blob = d_blob;
   a.X = d_X;
   a.n_rows = n_rows;
-  a.ld_x = ld_x;
+  a.row_stride = rs;
+  a.col_stride = cs;
   a.out = out;
   a.M = info->n_features;
   a.G = info->n_groups;
@@ -192,7 +194,7 @@ gts_status launch_bins(const gts_blob_info* info, const char* d_blob, const void
   return cuda_check("warp-bin kernel launch");
 }
 
-gts_status check_call(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows, int64_t ld_x,
+gts_status check_call(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows, int64_t rs, int64_t cs,
                       void* d_out) {
   if (!info) return fail(GTS_ERR_INVALID_ARGUMENT, "info is NULL");
   if (info->magic != kMagic || info->abi_version != GTS_ABI_VERSION)
@@ -203,7 +205,12 @@ gts_status check_call(const gts_blob_info* info, const void* d_blob, const void*
   if (n_rows < 0) return fail(GTS_ERR_INVALID_ARGUMENT, "n_rows < 0");
   if (n_rows == 0) return GTS_OK;
   if (!d_blob || !d_X || !d_out) return fail(GTS_ERR_INVALID_ARGUMENT, "NULL device pointer");
-  if (ld_x < info->n_features) return fail(GTS_ERR_INVALID_ARGUMENT, "ld_x < n_features");
+  const bool row_major = cs == 1 && rs >= info->n_features;
+  const bool feature_major = rs == 1 && cs >= n_rows;
+  if (!row_major && !feature_major)
+    return fail(GTS_ERR_INVALID_ARGUMENT,
+                "X strides (%lld, %lld): need row-major (col_stride 1, row_stride >= n_features) or "
+                "feature-major (row_stride 1, col_stride >= n_rows)", (long long)rs, (long long)cs);
   const size_t ts = info->dtype == GTS_F32 ? 4 : 8;
   if ((reinterpret_cast<uintptr_t>(d_blob) & 15) != 0) return fail(GTS_ERR_INVALID_ARGUMENT, "blob not 16-byte aligned");
   if ((reinterpret_cast<uintptr_t>(d_X) % ts) != 0 || (reinterpret_cast<uintptr_t>(d_out) % ts) != 0)
@@ -212,9 +219,9 @@ gts_status check_call(const gts_blob_info* info, const void* d_blob, const void*
 }
 
 template <bool kInter>
-gts_status run(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows, int64_t ld_x,
+gts_status run(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows, int64_t rs, int64_t cs,
                void* d_out, void* stream) {
-  gts_status s = check_call(info, d_blob, d_X, n_rows, ld_x, d_out);
+  gts_status s = check_call(info, d_blob, d_X, n_rows, rs, cs, d_out);
   if (s != GTS_OK || n_rows == 0) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const char* blob = static_cast<const char*>(d_blob);
@@ -223,10 +230,10 @@ gts_status run(const gts_blob_info* info, const void* d_blob, const void* d_X, i
           : launch_init<double>(kInter, info, blob, n_rows, d_out, st);
   if (s != GTS_OK) return s;
   if (info->layout == GTS_LAYOUT_NODAL)
-    return f32 ? launch_nodal_s<float, kInter>(info, blob, d_X, n_rows, ld_x, d_out, st)
-               : launch_nodal_s<double, kInter>(info, blob, d_X, n_rows, ld_x, d_out, st);
-  return f32 ? launch_bins<float, kInter>(info, blob, d_X, n_rows, ld_x, d_out, st)
-             : launch_bins<double, kInter>(info, blob, d_X, n_rows, ld_x, d_out, st);
+    return f32 ? launch_nodal_s<float, kInter>(info, blob, d_X, n_rows, rs, cs, d_out, st)
+               : launch_nodal_s<double, kInter>(info, blob, d_X, n_rows, rs, cs, d_out, st);
+  return f32 ? launch_bins<float, kInter>(info, blob, d_X, n_rows, rs, cs, d_out, st)
+             : launch_bins<double, kInter>(info, blob, d_X, n_rows, rs, cs, d_out, st);
 }
 
 }  // namespace
@@ -236,12 +243,23 @@ extern "C" {
 
 gts_status gts_shap(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows, int64_t ld_x,
                     void* d_phi, void* stream) {
-  return gts::run<false>(info, d_blob, d_X, n_rows, ld_x, d_phi, stream);
+  return gts::run<false>(info, d_blob, d_X, n_rows, ld_x, 1, d_phi, stream);
 }
 
 gts_status gts_shap_interactions(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
                                  int64_t ld_x, void* d_phi_ij, void* stream) {
-  return gts::run<true>(info, d_blob, d_X, n_rows, ld_x, d_phi_ij, stream);
+  return gts::run<true>(info, d_blob, d_X, n_rows, ld_x, 1, d_phi_ij, stream);
+}
+
+gts_status gts_shap_strided(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
+                            int64_t row_stride, int64_t col_stride, void* d_phi, void* stream) {
+  return gts::run<false>(info, d_blob, d_X, n_rows, row_stride, col_stride, d_phi, stream);
+}
+
+gts_status gts_shap_interactions_strided(const gts_blob_info* info, const void* d_blob, const void* d_X,
+                                         int64_t n_rows, int64_t row_stride, int64_t col_stride, void* d_phi_ij,
+                                         void* stream) {
+  return gts::run<true>(info, d_blob, d_X, n_rows, row_stride, col_stride, d_phi_ij, stream);
 }
 
 int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions) {

@@ -328,17 +328,22 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
 #pragma unroll
         for (int q = 0; q < Q; ++q) W[r][q] = h[q] * P[r][q];
     }
-    T u[R][KM][Q];
+    // u_s = (o_s - z_s)/f_s(t_q): cached in registers for small paths; for
+    // larger ones the partner's u is applied as a select on the dot product
+    constexpr bool kCacheU = Q <= 5;
+    T u[R][kCacheU ? KM : 1][Q];
+    if constexpr (kCacheU) {
 #pragma unroll
-    for (int s = 0; s < KM; ++s) {
-      if (s < KM - 1 || s < k) {
-        T al[Q];
-        lds_vec(al, tp + 3 * QP + s * 3 * QP + 2 * QP);
+      for (int s = 0; s < KM; ++s) {
+        if (s < KM - 1 || s < k) {
+          T al[Q];
+          lds_vec(al, tp + 3 * QP + s * 3 * QP + 2 * QP);
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const bool o = (om[r] >> s) & 1u;
+          for (int r = 0; r < R; ++r) {
+            const bool o = (om[r] >> s) & 1u;
 #pragma unroll
-          for (int q = 0; q < Q; ++q) u[r][s][q] = o ? al[q] : G[q];  // UNWIND(s) folded into u
+            for (int q = 0; q < Q; ++q) u[r][s][q] = o ? al[q] : G[q];  // UNWIND(s) folded into u
+          }
         }
       }
     }
@@ -346,26 +351,42 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
 #pragma unroll
     for (int i = 0; i < KM; ++i) {
       if (i < KM - 1 || i < k) {
-        T y[R][Q], phi[R];
+        T y[R][Q], phi[R], yg[R];
+        T ai[Q];
+        if constexpr (!kCacheU) lds_vec(ai, tp + 3 * QP + i * 3 * QP + 2 * QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          T a = (T)0;
+          T a = (T)0, g = (T)0;
+          const bool oi = (om[r] >> i) & 1u;
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
-            y[r][q] = W[r][q] * u[r][i][q];
+            T ui;
+            if constexpr (kCacheU) ui = u[r][i][q];
+            else ui = oi ? ai[q] : G[q];
+            y[r][q] = W[r][q] * ui;
             a += y[r][q];
+            if constexpr (!kCacheU) g = fma(y[r][q], G[q], g);
           }
           phi[r] = a + a;  // phi_i
+          yg[r] = g;
         }
         const int cdiag = c++;
 #pragma unroll
         for (int j = i + 1; j < KM; ++j) {
           if (j < KM - 1 || j < k) {
+            T aj[Q];
+            if constexpr (!kCacheU) lds_vec(aj, tp + 3 * QP + j * 3 * QP + 2 * QP);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               T v = (T)0;
+              if constexpr (kCacheU) {
 #pragma unroll
-              for (int q = 0; q < Q; ++q) v = fma(y[r][q], u[r][j][q], v);
+                for (int q = 0; q < Q; ++q) v = fma(y[r][q], u[r][j][q], v);
+              } else {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) v = fma(y[r][q], aj[q], v);
+                v = ((om[r] >> j) & 1u) ? v : yg[r];
+              }
               add(r, c, i, j, v);
             }
           }
@@ -530,7 +551,8 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
 struct Args {
   const char* blob;
   const void* X;
-  int64_t n_rows, ld_x;
+  int64_t n_rows;
+  int64_t row_stride, col_stride;  // X[r][f] at X[r * row_stride + f * col_stride]
   void* out;
   int n_splits;
   int M, G;
@@ -661,50 +683,81 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
   int64_t cur_map_begin = 0;
   bool dirty = false;
 
-  // one atomic per non-zero (row, group, feature) cell of this lane's tiles
+  // Warp-cooperative flush of the warp's tiles: lane = feature slot, rows walked
+  // in order, so consecutive lanes issue atomics to consecutive features of one
+  // row (coalesced RED) and the loads of the tile are independent (ILP).  One
+  // atomic per non-zero (row, group, feature) cell.
+  const int tile_row0 = warp * ROWS;
   auto flush = [&]() {
     if (dirty) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (!ok[r]) continue;
-        if constexpr (kInter) {
-          T* base = out + ((size_t)row[r] * a.G + cur_group) * (size_t)M1 * M1;
-          for (int i = 0; i < cur_slots; ++i) {
-            // the diagonal cell holds sum phi_i; Eq. 6: phi_ii = phi_i - sum_{j != i} phi_ij
-            T rowsum = (T)0;
-            for (int j = 0; j < cur_slots; ++j)
-              if (j != i) rowsum += sT[ab[r] + (j < i ? tri_row_base(j, S) + i : tri_row_base(i, S) + j)];
-            const int fi = slotmap[cur_map_begin + i];
-            const T d = sT[ab[r] + tri_row_base(i, S) + i] - rowsum;
-            if (d != (T)0) atomicAdd(base + (size_t)fi * M1 + fi, d);
-          }
-          for (int i = 0; i < cur_slots; ++i) {
-            const int fi = slotmap[cur_map_begin + i];
-            const int rb = tri_row_base(i, S);
-            sT[ab[r] + rb + i] = (T)0;
-            for (int j = i + 1; j < cur_slots; ++j) {
-              const T v = sT[ab[r] + rb + j];
-              if (v != (T)0) {
-                const int fj = slotmap[cur_map_begin + j];
-                atomicAdd(base + (size_t)fi * M1 + fj, v);
-                atomicAdd(base + (size_t)fj * M1 + fi, v);
-                sT[ab[r] + rb + j] = (T)0;
+      __syncwarp();
+      const int total = ROWS * cur_slots;  // (row, slot) pairs, slot fastest
+      for (int idx = lane; idx < total; idx += 32) {
+        const int rr = idx / cur_slots, i = idx - rr * cur_slots;
+        const int fi = slotmap[cur_map_begin + i];
+        {
+          const int64_t rg = row0 + rr;
+          T* tile = sT + o_acc + (tile_row0 + rr) * AS;
+          if constexpr (kInter) {
+            const int rbi = tri_row_base(i, S);
+            if (rg < a.n_rows) {
+              T* base = out + ((size_t)rg * a.G + cur_group) * (size_t)M1 * M1;
+              // the diagonal cell holds sum phi_i; Eq. 6: phi_ii = phi_i - sum_{j != i} phi_ij
+              T rowsum = (T)0;
+              for (int j = 0; j < cur_slots; ++j)
+                if (j != i) rowsum += tile[j < i ? tri_row_base(j, S) + i : rbi + j];
+              const T d = tile[rbi + i] - rowsum;
+              if (d != (T)0) atomicAdd(base + (size_t)fi * M1 + fi, d);
+              for (int j = i + 1; j < cur_slots; ++j) {
+                const T v = tile[rbi + j];
+                if (v != (T)0) {
+                  const int fj = slotmap[cur_map_begin + j];
+                  atomicAdd(base + (size_t)fi * M1 + fj, v);
+                  atomicAdd(base + (size_t)fj * M1 + fi, v);
+                }
               }
             }
-          }
-        } else {
-          T* base = out + ((size_t)row[r] * a.G + cur_group) * (size_t)M1;
-          for (int i = 0; i < cur_slots; ++i) {
-            const T v = sT[ab[r] + i];
-            if (v != (T)0) {
-              atomicAdd(base + slotmap[cur_map_begin + i], v);
-              sT[ab[r] + i] = (T)0;
-            }
+          } else {
+            const T v = tile[i];
+            if (rg < a.n_rows && v != (T)0) atomicAdd(out + ((size_t)rg * a.G + cur_group) * (size_t)M1 + fi, v);
           }
         }
       }
+      __syncwarp();
+      // zero the tiles (interaction rows are read across lanes above, so only now)
+      for (int idx = lane; idx < ROWS * AW; idx += 32) sT[o_acc + (tile_row0 + idx / AW) * AS + idx % AW] = (T)0;
+      __syncwarp();
     }
     dirty = false;
+  };
+
+  // Warp-cooperative gather of X into slot order: lane = slot, so each load
+  // instruction reads one row's features (contiguous for identity maps).
+  auto gather = [&](const ChunkRec& c) {
+    __syncwarp();
+    if (a.col_stride == 1) {
+      // row-major X: lane = slot, each load instruction reads one row
+      for (int i = lane; i < c.n_slots; i += 32) {
+        const int f = slotmap[c.slotmap_begin + i];
+#pragma unroll 8
+        for (int rr = 0; rr < ROWS; ++rr) {
+          const int64_t rg = row0 + rr;
+          sT[o_x + (tile_row0 + rr) * XS + i] = rg < a.n_rows ? X[(size_t)rg * a.row_stride + f] : (T)0;
+        }
+      }
+    } else {
+      // feature-major X: lane = row, each load instruction reads 32 consecutive rows of one feature
+#pragma unroll 4
+      for (int i = 0; i < c.n_slots; ++i) {
+        const size_t fo = (size_t)slotmap[c.slotmap_begin + i] * a.col_stride;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int64_t rg = row0 + r * 32 + lane;
+          sT[o_x + (tile_row0 + r * 32 + lane) * XS + i] = rg < a.n_rows ? X[fo + (size_t)rg * a.row_stride] : (T)0;
+        }
+      }
+    }
+    __syncwarp();
   };
 
   uint32_t phase[2] = {0u, 0u};
@@ -719,12 +772,7 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
     }
     if (c.map_id != cur_map || c.group != cur_group) {
       flush();
-      if (c.map_id != cur_map) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          for (int i = 0; i < c.n_slots; ++i)
-            sT[xb[r] + i] = ok[r] ? X[(size_t)row[r] * a.ld_x + slotmap[c.slotmap_begin + i]] : (T)0;
-      }
+      if (c.map_id != cur_map) gather(c);
       cur_map = c.map_id;
       cur_group = c.group;
       cur_slots = c.n_slots;

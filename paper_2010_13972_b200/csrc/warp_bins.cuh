@@ -101,7 +101,8 @@ __device__ __forceinline__ void seg_atomic_add(bool active, K key, T val, T* add
 struct BinArgs {
   const char* blob;
   const void* X;
-  int64_t n_rows, ld_x;
+  int64_t n_rows;
+  int64_t row_stride, col_stride;
   void* out;
   int M, G;
   int64_t n_bins;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(W * 32) bins_shap_kernel(BinArgs a) {
     T o = (T)0;
     if (feat == -1) o = (T)1;  // root: irrelevant to every output (reading G6)
     else if (feat >= 0) {
-      const T x = X[row * a.ld_x + feat];
+      const T x = X[row * a.row_stride + (int64_t)feat * a.col_stride];
       o = (x >= (T)lo && x < (T)hi) ? (T)1 : (T)0;  // GetOneFraction
     }
     const T w = warp_extend<T>(feat >= -1 ? rank : 99, K, base, z, o, kmax, -1);
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(W * 32) bins_inter_kernel(BinArgs a) {
     T o0 = (T)0;
     if (feat0 == -1) o0 = (T)1;
     else if (feat0 >= 0) {
-      const T x = X[row * a.ld_x + feat0];
+      const T x = X[row * a.row_stride + (int64_t)feat0 * a.col_stride];
       o0 = (x >= (T)lo && x < (T)hi) ? (T)1 : (T)0;
     }
     T* rowbase = out + ((size_t)row * a.G + grp) * (size_t)M1 * M1;

@@ -90,13 +90,24 @@ class TreeShapExplainer:
             X = X.contiguous()
         return X
 
+    @staticmethod
+    def _strides(X: torch.Tensor):
+        """(row_stride, col_stride) of a row-major or feature-major [n][M] view."""
+        n, m = X.shape
+        if X.stride(1) == 1 or m == 1:
+            return X.stride(0) if n > 1 else max(m, 1), 1
+        if X.stride(0) == 1:
+            return 1, X.stride(1)
+        raise ValueError("X must be row-major or feature-major (one unit stride)")
+
     def shap_device(self, X: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        """phi [n_rows][G][M+1] on the device (X already on the device)."""
+        """phi [n_rows][G][M+1] on the device (X already on the device, row- or feature-major)."""
         n = X.shape[0]
         if out is None:
             out = torch.empty((n, self.n_groups, self.n_features + 1), dtype=self.torch_dtype, device=self.device)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        gts.gts_shap(self.blob.info, self.blob.ptr, X.data_ptr(), n, X.stride(0), out.data_ptr(), st.cuda_stream)
+        rs, cs = self._strides(X)
+        gts.gts_shap_strided(self.blob.info, self.blob.ptr, X.data_ptr(), n, rs, cs, out.data_ptr(), st.cuda_stream)
         return out
 
     def interactions_device(self, X: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
@@ -106,8 +117,9 @@ class TreeShapExplainer:
         if out is None:
             out = torch.empty((n, self.n_groups, M1, M1), dtype=self.torch_dtype, device=self.device)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        gts.gts_shap_interactions(self.blob_int.info, self.blob_int.ptr, X.data_ptr(), n, X.stride(0),
-                                  out.data_ptr(), st.cuda_stream)
+        rs, cs = self._strides(X)
+        gts.gts_shap_interactions_strided(self.blob_int.info, self.blob_int.ptr, X.data_ptr(), n, rs, cs,
+                                          out.data_ptr(), st.cuda_stream)
         return out
 
     # ------------------------------------------------------------------- host

@@ -76,6 +76,7 @@ class gts_blob_info(ctypes.Structure):
 # The symbols the header declares (checked by tests/test_abi.py).
 EXPORTS = ["gts_extract_paths", "gts_paths_view_get", "gts_paths_free", "gts_binpack", "gts_bins_view_get",
            "gts_bins_free", "gts_blob_plan", "gts_blob_write", "gts_shap", "gts_shap_interactions",
+           "gts_shap_strided", "gts_shap_interactions_strided",
            "gts_launches_per_call", "gts_last_error", "gts_status_string", "gts_abi_version"]
 
 _lib = None
@@ -104,6 +105,10 @@ def load(path: str = LIB_PATH):
     for name in ("gts_shap", "gts_shap_interactions"):
         fn = getattr(lib, name)
         fn.argtypes = [P(gts_blob_info), _vp, _vp, _i64, _i64, _vp, _vp]
+    for name in ("gts_shap_strided", "gts_shap_interactions_strided"):
+        fn = getattr(lib, name)
+        fn.argtypes = [P(gts_blob_info), _vp, _vp, _i64, _i64, _i64, _vp, _vp]
+        fn.restype = ctypes.c_int
     lib.gts_launches_per_call.argtypes = [P(gts_blob_info), _i32]
     lib.gts_launches_per_call.restype = _i32
     lib.gts_last_error.argtypes = []
@@ -234,6 +239,20 @@ def gts_shap_interactions(info: gts_blob_info, d_blob: int, d_x: int, n_rows: in
     """(4) SHAP interaction values."""
     _check(load().gts_shap_interactions(ctypes.byref(info), d_blob, d_x, int(n_rows), int(ld_x), d_phi_ij,
                                         stream or None))
+
+
+def gts_shap_strided(info: gts_blob_info, d_blob: int, d_x: int, n_rows: int, row_stride: int, col_stride: int,
+                     d_phi: int, stream: int = 0):
+    """(3) SHAP values for X[r][f] at d_x[r * row_stride + f * col_stride]."""
+    _check(load().gts_shap_strided(ctypes.byref(info), d_blob, d_x, int(n_rows), int(row_stride), int(col_stride),
+                                   d_phi, stream or None))
+
+
+def gts_shap_interactions_strided(info: gts_blob_info, d_blob: int, d_x: int, n_rows: int, row_stride: int,
+                                  col_stride: int, d_phi_ij: int, stream: int = 0):
+    """(4) SHAP interaction values, strided X."""
+    _check(load().gts_shap_interactions_strided(ctypes.byref(info), d_blob, d_x, int(n_rows), int(row_stride),
+                                                int(col_stride), d_phi_ij, stream or None))
 
 
 def gts_launches_per_call(info: gts_blob_info, interactions: bool) -> int:

@@ -229,3 +229,27 @@ def test_local_accuracy_full_size(gpu):
     phi_ij = ex.interactions_device(xd).cpu().numpy()
     parity.check(phi_ij[sub], oracle.interactions(ens, x[sub].astype(np.float64)), "f32", "sampled interactions")
     np.testing.assert_allclose(phi_ij[:, 0, :8, :8].sum(axis=2), phi[:, 0, :8], atol=2e-4)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("name", ["cal_housing-med", "fashion_mnist-med"])
+def test_feature_major_x(gpu, layout, name):
+    """X given feature-major (gts_shap_strided with row_stride 1) gives the same
+    results as row-major; padded column stride and a ragged row count."""
+    import torch
+    w = WORKLOADS[name]
+    ens = w.ensemble().subset(range(60))
+    n = 333
+    x = w.x(n, ens=ens)
+    xt = np.zeros((w.n_features, n + 7), np.float32)
+    xt[:, :n] = x.T
+    xd = torch.from_numpy(xt).cuda()[:, :n].t()  # shape [n][M], strides (1, n + 7)
+    ex = _explainer(ens, "f32", layout, interactions=(w.n_features <= 16))
+    phi = ex.shap_device(xd)
+    torch.cuda.synchronize()
+    parity.check(phi.cpu().numpy(), oracle.treeshap(ens, x.astype(np.float64)), "f32", "feature-major shap")
+    if w.n_features <= 16:
+        pij = ex.interactions_device(xd[:40])
+        torch.cuda.synchronize()
+        parity.check(pij.cpu().numpy(), oracle.interactions(ens, x[:40].astype(np.float64)), "f32",
+                     "feature-major interactions")
