@@ -94,10 +94,12 @@ class TreeShapExplainer:
     def _strides(X: torch.Tensor):
         """(row_stride, col_stride) of a row-major or feature-major [n][M] view."""
         n, m = X.shape
+        if X.numel() == 0:
+            return max(m, 1), 1
         if X.stride(1) == 1 or m == 1:
-            return X.stride(0) if n > 1 else max(m, 1), 1
-        if X.stride(0) == 1:
-            return 1, X.stride(1)
+            return (X.stride(0) if n > 1 else m), 1
+        if X.stride(0) == 1 or n == 1:
+            return 1, (X.stride(1) if m > 1 else n)
         raise ValueError("X must be row-major or feature-major (one unit stride)")
 
     def shap_device(self, X: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
