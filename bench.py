@@ -51,6 +51,13 @@ def parse():
     ap.add_argument("--pack", default="bfd")
     ap.add_argument("--x-layout", choices=["row", "feature"], default="row",
                     help="X row-major [n][M] or feature-major (gts_shap_strided, row_stride 1)")
+    ap.add_argument("--phi-ij-budget-gb", type=int, default=48,
+                    help="device bytes for phi_ij; larger outputs are streamed in row chunks")
+    ap.add_argument("--ablation-rows", type=int, default=1 << 16)
+    ap.add_argument("--pack-ablation", action="store_true",
+                    help="ablation: warp-bin SHAP kernel with every packer (bfd, ffd, nf, none)")
+    ap.add_argument("--latency-sweep", action="store_true",
+                    help="row-count sweep 1..rows-per-gpu: eager vs CUDA-graph call latency beside the oracle")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ablation", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -284,7 +291,11 @@ def run_ours(args):
     x_rs, x_cs = TreeShapExplainer._strides(xd)
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     phi = torch.empty((n, G, M + 1), dtype=tdt, device=dev) if do_shap else None
-    phi_ij = torch.empty((n, G, M + 1, M + 1), dtype=tdt, device=dev) if do_int else None
+    # wide models (fashion_mnist: 24.6 MB of phi_ij per row) stream the rows in
+    # chunks through one reused buffer; otherwise one call
+    ij_row_bytes = G * (M + 1) ** 2 * (4 if args.dtype == "f32" else 8)
+    ij_chunk = n if not do_int else max(1, min(n, (args.phi_ij_budget_gb << 30) // ij_row_bytes))
+    phi_ij = torch.empty((ij_chunk, G, M + 1, M + 1), dtype=tdt, device=dev) if do_int else None
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -296,8 +307,10 @@ def run_ours(args):
             if evs: evs[1].record(stream)
         if do_int:
             if evs: evs[2].record(stream)
-            gts.gts_shap_interactions_strided(info_i, ex.blob_int.ptr, xd.data_ptr(), n, x_rs, x_cs, phi_ij.data_ptr(),
-                                      stream.cuda_stream)
+            for r0 in range(0, n, ij_chunk):
+                xr = xd[r0:r0 + ij_chunk]
+                gts.gts_shap_interactions_strided(info_i, ex.blob_int.ptr, xr.data_ptr(), xr.shape[0], x_rs, x_cs,
+                                                  phi_ij.data_ptr(), stream.cuda_stream)
             if evs: evs[3].record(stream)
 
     for _ in range(args.warmup):
@@ -331,7 +344,8 @@ def run_ours(args):
     if not args.no_e2e:
         x_pin = xt.pin_memory()
         phi_h = torch.empty(phi.shape, dtype=tdt, pin_memory=True) if do_shap else None
-        phi_ij_h = torch.empty(phi_ij.shape, dtype=tdt, pin_memory=True) if do_int else None
+        e2e_chunk = max(1, min(ij_chunk, (4 << 30) // ij_row_bytes))  # pinned host staging <= 4 GiB
+        phi_ij_h = torch.empty((e2e_chunk,) + tuple(phi_ij.shape[1:]), dtype=tdt, pin_memory=True) if do_int else None
         xe = torch.empty_like(xd)
 
         def e2e_step():
@@ -340,8 +354,8 @@ def run_ours(args):
                 ex.shap_device(xe, out=phi, stream=stream)
                 phi_h.copy_(phi, non_blocking=True)
             if do_int:
-                ex.interactions_device(xe, out=phi_ij, stream=stream)
-                phi_ij_h.copy_(phi_ij, non_blocking=True)
+                for r0, r1, chunk in ex.iter_interactions(xe, e2e_chunk, stream=stream, n_buffers=1):
+                    phi_ij_h[: r1 - r0].copy_(chunk, non_blocking=True)
 
         for _ in range(2):
             e2e_step()
@@ -358,8 +372,7 @@ def run_ours(args):
             te.append(a.elapsed_time(b))
         ms_e2e = max_over_ranks(float(np.mean(te)), world)
         h2d = xt.numel() * xt.element_size()
-        d2h = (phi.numel() * phi.element_size() if do_shap else 0) + (
-            phi_ij.numel() * phi_ij.element_size() if do_int else 0)
+        d2h = (phi.numel() * phi.element_size() if do_shap else 0) + (n * ij_row_bytes if do_int else 0)
         e2e = {"value": world * n / (ms_e2e / 1000.0), "unit": "rows/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e,
                "api": "TreeShapExplainer.shap_device/interactions_device with pinned host X and phi (H2D + D2H)"}
@@ -367,25 +380,40 @@ def run_ours(args):
     # --- ablation: the paper-lineage warp-bin kernels on a slice of the rows
     ablation = None
     if not args.no_ablation and rank == 0:
-        na = min(n, 1 << 16)
-        exb = TreeShapExplainer(ens, dtype=args.dtype, pack=args.pack, layout="warp_bins", device=dev,
-                                interactions=do_int)
+        # the paper-lineage warp-bin kernels on a slice of the rows; with
+        # --pack-ablation every packer's bins (utilisation ->
+        # kernel time), SHAP only
+        na = min(n, args.ablation_rows)
         xa = xd[:na]
-        res = {}
-        for name, fn, on in (("shap", exb.shap_device, do_shap), ("interactions", exb.interactions_device, do_int)):
-            if not on:
-                continue
-            fn(xa)
+        res = {"rows": na, "layout": "warp_bins (paper lineage: lane per path element, shuffles, swap-to-end)"}
+
+        def timed(fn, x):
+            fn(x)
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            fn(xa)
+            fn(x)
             b.record(stream)
             torch.cuda.synchronize()
-            res[name + "_rows_per_s"] = na / (a.elapsed_time(b) / 1000.0)
-        bv = exb.bins.view()
-        res.update({"rows": na, "bins": int(bv["n_bins"]), "utilisation": bv["utilisation"],
-                    "layout": "warp_bins (paper lineage: lane per path element, shuffles, swap-to-end)"})
+            return x.shape[0] / (a.elapsed_time(b) / 1000.0)
+
+        packs = ["bfd", "ffd", "nf", "none"] if args.pack_ablation else [args.pack]
+        for pk in packs:
+            exb = TreeShapExplainer(ens, dtype=args.dtype, pack=pk, layout="warp_bins", device=dev,
+                                    interactions=do_int and pk == args.pack)
+            bv = exb.bins.view()
+            ent = {"bins": int(bv["n_bins"]), "utilisation": bv["utilisation"]}
+            if do_shap:
+                ent["shap_rows_per_s"] = timed(exb.shap_device, xa)
+            if do_int and pk == args.pack:
+                ni = max(1, min(na, ij_chunk, 8192))
+                ent["interactions_rows_per_s"] = timed(exb.interactions_device, xa[:ni])
+                ent["interaction_rows"] = ni
+            if pk == args.pack:
+                res.update(ent)
+            if args.pack_ablation:
+                res.setdefault("packers", {})[pk] = ent
+            del exb
         ablation = res
 
     cpu = None
@@ -432,7 +460,7 @@ def run_ours(args):
         except Exception:
             pass
     launches = (gts.gts_launches_per_call(info_s, False) if do_shap else 0) + (
-        gts.gts_launches_per_call(info_i, True) if do_int else 0)
+        gts.gts_launches_per_call(info_i, True) * -(-n // ij_chunk) if do_int else 0)
     line = {
         "metric": METRIC,
         "value": total_rows / (ms_step / 1000.0),
@@ -451,6 +479,7 @@ def run_ours(args):
                    "paths": int(info_s.n_paths), "path_elems": int(info_s.n_elems), "layout": args.layout,
                    "pack": args.pack, "x_layout": args.x_layout, "bins": int(bins_view["n_bins"]),
                    "bin_utilisation": round(float(bins_view["utilisation"]), 6),
+                   "phi_ij_chunk_rows": ij_chunk if do_int else None,
                    "l2": "flushed between timed steps (512 MiB memset outside the events); phi_ij > L2",
                    "parallelism": f"dp{world}: rows sharded, path table replicated by one NCCL broadcast"},
         "shap": {"rows_per_s": total_rows / (ms_shap / 1000.0), "ms": ms_shap, "roofline": r_shap} if do_shap else None,
@@ -476,8 +505,81 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_sweep(args):
+    """Latency regime (Fig. 4): per row
+    count, the device time of one SHAP call issued eagerly (init + main kernel
+    launches through the C ABI) and replayed from a CUDA graph, beside the
+    oracle (fp64, all host cores) on the same rows; prints one JSON line."""
+    import torch
+
+    import oracle
+    from paper_2010_13972_b200.explainer import TreeShapExplainer
+    from synth.configs import WORKLOADS
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    w = WORKLOADS[args.workload]
+    ens = w.ensemble()
+    ex = TreeShapExplainer(ens, dtype=args.dtype, pack=args.pack, layout=args.layout, device=dev,
+                           interactions=False)
+    stream = torch.cuda.current_stream(dev)
+    points = []
+    n_max = int(args.rows_per_gpu)
+    counts = [c for c in (1, 4, 16, 64, 256, 1024, 4096, 16384, 65536, 262144, 1 << 20) if c <= n_max]
+    x_all = w.x(max(counts), ens=ens if w.tie_frac > 0 else None)
+    xd_all = torch.from_numpy(x_all if args.dtype == "f32" else x_all.astype(np.float64)).to(dev)
+    for n in counts:
+        xd = xd_all[:n]
+        out = torch.empty((n, w.n_groups, w.n_features + 1), dtype=xd.dtype, device=dev)
+        reps = 50 if n <= 4096 else (10 if n <= 65536 else 3)
+
+        def timed(fn):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b) * 1000.0)
+            return float(np.median(ts))
+
+        # eager: back-to-back calls so the host launch cost is part of the device timeline
+        eager = timed(lambda: ex.shap_device(xd, out=out, stream=stream))
+        g = ex.graphed(n)
+        g.x.copy_(xd)
+        graph = timed(g.replay)
+        del g
+        cpu_us = None
+        if n <= 4096:
+            xr = x_all[:n].astype(np.float64)
+            t0 = time.perf_counter()
+            r = 0
+            while True:
+                oracle.treeshap(ens, xr)
+                r += 1
+                if time.perf_counter() - t0 > 0.2 or r >= 20:
+                    break
+            cpu_us = (time.perf_counter() - t0) / r * 1e6
+        points.append({"rows": n, "eager_us": eager, "graph_us": graph, "cpu_oracle_us": cpu_us,
+                       "graph_rows_per_s": n / (graph * 1e-6)})
+    cross = next((p["rows"] for p in points if p["cpu_oracle_us"] is not None and p["cpu_oracle_us"] > p["graph_us"]),
+                 None)
+    print(json.dumps({"sweep": "latency", "workload": args.workload, "dtype": args.dtype, "layout": args.layout,
+                      "points": points, "gpu_faster_from_rows": cross,
+                      "cpu_cores": oracle.num_threads(),
+                      "note": "device time per SHAP call (CUDA events, median); cpu = fp64 oracle wall time"}),
+          flush=True)
+
+
 def main():
     args = parse()
+    if args.latency_sweep:
+        run_sweep(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -124,6 +124,36 @@ class TreeShapExplainer:
                                           out.data_ptr(), st.cuda_stream)
         return out
 
+    def graphed(self, n_rows: int, interactions: bool = False) -> "GraphedCall":
+        """Latency regime: capture one call for
+        a fixed row count into a CUDA graph over static X / output buffers, so
+        a small batch costs one graph launch instead of two kernel launches
+        plus argument checks."""
+        return GraphedCall(self, n_rows, interactions)
+
+    def interaction_bytes_per_row(self) -> int:
+        return self.n_groups * (self.n_features + 1) ** 2 * torch.tensor([], dtype=self.torch_dtype).element_size()
+
+    def iter_interactions(self, X: torch.Tensor, chunk_rows: int, stream=None, n_buffers: int = 2):
+        """Row-chunked streaming of phi_ij for wide models:
+        fashion_mnist-shaped models need 24.6 MB of phi_ij per row, so the rows
+        are explained in chunks of `chunk_rows` into `n_buffers` rotating device
+        buffers.  Yields (row0, row1, phi_ij_chunk) with the chunk's kernel
+        enqueued on `stream`; a buffer is reused only after the work the caller
+        enqueued on `stream` after the yield (e.g. a D2H copy or a reduction)
+        has been ordered before it, since everything runs on the one stream."""
+        n = X.shape[0]
+        M1 = self.n_features + 1
+        chunk_rows = max(1, min(int(chunk_rows), max(n, 1)))
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        bufs = [torch.empty((chunk_rows, self.n_groups, M1, M1), dtype=self.torch_dtype, device=self.device)
+                for _ in range(min(n_buffers, max(1, -(-n // chunk_rows))))]
+        for i, r0 in enumerate(range(0, n, chunk_rows)):
+            r1 = min(n, r0 + chunk_rows)
+            out = bufs[i % len(bufs)][: r1 - r0]
+            self.interactions_device(X[r0:r1], out=out, stream=st)
+            yield r0, r1, out
+
     # ------------------------------------------------------------------- host
     def shap(self, X) -> np.ndarray:
         """End to end from host X: H2D, kernels, D2H of phi."""
@@ -133,3 +163,31 @@ class TreeShapExplainer:
     def shap_interactions(self, X) -> np.ndarray:
         Xd = self._device_x(X)
         return self.interactions_device(Xd).cpu().numpy()
+
+
+class GraphedCall:
+    """One gts_shap / gts_shap_interactions call captured in a CUDA graph.
+
+    Copy the rows into ``x`` (static [n_rows][M] device buffer), ``replay()``,
+    read ``out``.  The captured kernels are the library's own (init + main)."""
+
+    def __init__(self, ex: TreeShapExplainer, n_rows: int, interactions: bool = False):
+        self.ex = ex
+        M, G = ex.n_features, ex.n_groups
+        self.x = torch.zeros((n_rows, M), dtype=ex.torch_dtype, device=ex.device)
+        shape = (n_rows, G, M + 1, M + 1) if interactions else (n_rows, G, M + 1)
+        self.out = torch.empty(shape, dtype=ex.torch_dtype, device=ex.device)
+        fn = ex.interactions_device if interactions else ex.shap_device
+        side = torch.cuda.Stream(ex.device)
+        side.wait_stream(torch.cuda.current_stream(ex.device))
+        with torch.cuda.stream(side):  # warm-up outside capture (sets kernel attributes)
+            fn(self.x, out=self.out, stream=side)
+        torch.cuda.current_stream(ex.device).wait_stream(side)
+        torch.cuda.synchronize(ex.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            fn(self.x, out=self.out, stream=torch.cuda.current_stream(ex.device))
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.out

@@ -9,6 +9,7 @@ run cal_housing-med cal_housing-med --rows-per-gpu 1048576 --steps 10 ${EXTRA:-}
 run adult-large adult-large --rows-per-gpu 65536 --steps 5 ${EXTRA:-}
 run fashion_mnist-med fashion_mnist-med --rows-per-gpu 65536 --steps 5 --mode shap --x-layout feature ${EXTRA:-}
 run fashion_mnist-med-rowmajor fashion_mnist-med --rows-per-gpu 65536 --steps 5 --mode shap --no-ablation ${EXTRA:-}
+run fashion_mnist-med-int fashion_mnist-med --rows-per-gpu 10000 --steps 3 --mode interactions --no-ablation ${EXTRA:-}
 run covtype-large covtype-large --rows-per-gpu 32768 --steps 3 --mode shap ${EXTRA:-}
 run covtype-large-int covtype-large --rows-per-gpu 8192 --steps 3 --mode interactions --no-ablation ${EXTRA:-}
 run depth3-single depth3-single --rows-per-gpu 100 --steps 20 --no-ablation --no-e2e ${EXTRA:-}

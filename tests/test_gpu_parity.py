@@ -253,3 +253,21 @@ def test_feature_major_x(gpu, layout, name):
         torch.cuda.synchronize()
         parity.check(pij.cpu().numpy(), oracle.interactions(ens, x[:40].astype(np.float64)), "f32",
                      "feature-major interactions")
+
+
+@pytest.mark.parametrize("inter", [False, True])
+def test_graphed_call_small_batches(gpu, inter):
+    """Latency regime: the CUDA-graph replay of one call gives the oracle's
+    values for new rows copied into the static buffer (1, 7 and 300 rows)."""
+    w = WORKLOADS["cal_housing-small"]
+    ens = w.ensemble()
+    ex = _explainer(ens, "f32", "nodal")
+    import torch
+    for n in (1, 7, 300):
+        g = ex.graphed(n, interactions=inter)
+        for seed_row in (0, 5000):
+            x = w.x(n, row0=seed_row, ens=ens)
+            g.x.copy_(torch.from_numpy(x))
+            got = g.replay().cpu().numpy()
+            ref = (oracle.interactions if inter else oracle.treeshap)(ens, x.astype(np.float64))
+            parity.check(got, ref, "f32", f"graphed n={n} inter={inter}")
