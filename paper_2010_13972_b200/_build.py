@@ -15,7 +15,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libgts.so")
 SOURCES = [os.path.join(CSRC, "host.cpp"), os.path.join(CSRC, "kernels.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "blob_format.h"), os.path.join(ROOT, "include", "gts.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("blob_format.h", "nodal.cuh", "warp_bins.cuh")] + [
+    os.path.join(ROOT, "include", "gts.h")]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
@@ -40,14 +41,16 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libgts.so (or, with `out`/`defines`, a kernel variant for experiments)."""
+    lib = os.path.abspath(out) if out else LIB
+    if not force and out is None and not stale():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES, "-lgomp"]
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp, *SOURCES, "-lgomp"]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
-    log = os.path.join(LIB_DIR, "build.log")
+    log = os.path.join(LIB_DIR, "build.log" if out is None else os.path.basename(lib) + ".log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
@@ -55,8 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

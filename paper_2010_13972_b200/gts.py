@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libgts.so")
+# GTS_LIB selects another in-tree build of the same sources (kernel-variant experiments)
+LIB_PATH = os.environ.get("GTS_LIB") or os.path.join(_HERE, "_lib", "libgts.so")
 
 GTS_OK = 0
 STATUS_NAMES = {0: "GTS_OK", 1: "GTS_ERR_INVALID_ARGUMENT", 2: "GTS_ERR_INVALID_MODEL",
