@@ -33,7 +33,10 @@ def launch_shares(path):
 
 def rep_traffic(rep):
     """{kernel name: [dram read+write bytes per launch, ...]} from an ncu report."""
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".raw.csv"):
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     if len(rows) < 3:
         return {}
@@ -65,8 +68,11 @@ def main():
         shutil.copy(p, os.path.join(dst, f))
     tfile = os.path.join(os.path.dirname(dst.rstrip("/")), "traffic.json")
     traffic = json.load(open(tfile)) if os.path.exists(tfile) else {}
-    for rep in sorted(f for f in os.listdir(src) if f.endswith(".ncu-rep")):
+    reps = [f for f in os.listdir(src) if f.endswith(".ncu-rep")]
+    reps += [f for f in os.listdir(src) if f.endswith(".raw.csv") and f[:-8] + ".ncu-rep" not in reps]
+    for rep in sorted(reps):
         tr = rep_traffic(os.path.join(src, rep))
+        rep = rep[:-8] + ".ncu-rep" if rep.endswith(".raw.csv") else rep
         for key, rx in keys:
             for kname, vals in tr.items():
                 if re.search(rx, kname) and vals and all(v == v for v in vals):
