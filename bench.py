@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
     ap.add_argument("--layout", choices=["nodal", "warp_bins"], default="nodal")
     ap.add_argument("--pack", default="bfd")
+    ap.add_argument("--max-slots", type=int, default=0,
+                    help="NODAL slot width (0 = library choice: identity map up to 64 features)")
     ap.add_argument("--x-layout", choices=["row", "feature"], default="row",
                     help="X row-major [n][M] or feature-major (gts_shap_strided, row_stride 1)")
     ap.add_argument("--phi-ij-budget-gb", type=int, default=48,
@@ -258,10 +260,10 @@ def run_ours(args):
     t0 = time.perf_counter()
     if rank == 0:
         ex = TreeShapExplainer(ens, dtype=args.dtype, pack=args.pack, layout=args.layout, device=dev,
-                               interactions=do_int)
+                               interactions=do_int, max_slots=args.max_slots)
     else:
         ex = TreeShapExplainer(ens, dtype=args.dtype, pack=args.pack, layout=args.layout, device=dev,
-                               interactions=do_int, build_blobs=False)
+                               interactions=do_int, build_blobs=False, max_slots=args.max_slots)
         ex.blob = Blob(None, torch.empty(0, dtype=torch.uint8, device=dev))
         ex.blob_int = Blob(None, torch.empty(0, dtype=torch.uint8, device=dev)) if do_int else None
     torch.cuda.synchronize()
@@ -477,7 +479,7 @@ def run_ours(args):
         "config": {"workload": args.workload, "mode": args.mode, "rows_per_gpu": n, "global_rows": total_rows,
                    "trees": w.n_trees, "max_depth": w.max_depth, "features": M, "groups": G,
                    "paths": int(info_s.n_paths), "path_elems": int(info_s.n_elems), "layout": args.layout,
-                   "pack": args.pack, "x_layout": args.x_layout, "bins": int(bins_view["n_bins"]),
+                   "pack": args.pack, "x_layout": args.x_layout, "max_slots": int(info_s.max_slots), "bins": int(bins_view["n_bins"]),
                    "bin_utilisation": round(float(bins_view["utilisation"]), 6),
                    "phi_ij_chunk_rows": ij_chunk if do_int else None,
                    "l2": "flushed between timed steps (512 MiB memset outside the events); phi_ij > L2",

@@ -6,11 +6,12 @@ OUT=gpurun_out/${TAG:-ab}
 mkdir -p $OUT
 for lib in ${LIBS:-libgts.so}; do
   for spec in ${WLS:-cal_housing-med:both:1048576}; do
-    IFS=: read wl mode rows <<< "$spec"
+    IFS=: read wl mode rows slots <<< "$spec"
+    slots=${slots:-0}
     GTS_LIB=$PWD/paper_2010_13972_b200/_lib/$lib timeout 900 python bench.py --workload $wl --mode $mode \
-      --rows-per-gpu $rows --steps ${STEPS:-5} --no-cpu-baseline --no-e2e --no-ablation > $OUT/${lib%.so}_${wl}_$mode.json 2> $OUT/${lib%.so}_${wl}_$mode.err
-    echo "$lib $wl $mode rc=$?"
-    python - $OUT/${lib%.so}_${wl}_$mode.json <<'PY'
+      --rows-per-gpu $rows --max-slots $slots --steps ${STEPS:-5} --no-cpu-baseline --no-e2e --no-ablation ${EXTRA:-} > $OUT/${lib%.so}_${wl}_${mode}_s$slots.json 2> $OUT/${lib%.so}_${wl}_${mode}_s$slots.err
+    echo "$lib $wl $mode slots=$slots rc=$?"
+    python - $OUT/${lib%.so}_${wl}_${mode}_s$slots.json <<'PY'
 import json, sys
 try:
     d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
