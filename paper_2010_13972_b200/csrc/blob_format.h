@@ -44,7 +44,7 @@ static_assert(sizeof(BlobHeader) == 256, "header size");
 // NODAL: a chunk = consecutive paths of one group that touch at most max_slots
 // distinct features; a warp walks all of a chunk's paths for its rows.  Its
 // staged region (copied to shared memory with one TMA bulk copy) is
-//   int4 elem[n_elems]  {slot, lower bits, upper bits, tri-row base of slot}
+//   int4 elem[n_elems]  {lower bits, upper bits, slot, tri-row base of slot}
 //   int4 path[n_paths]  {k | run length << 16, Q, first elem, first table word}
 //   T    table[table_words]   (per path, see below)
 struct ChunkRec {              // 64 bytes
@@ -88,7 +88,8 @@ struct ElemRec {
 //   h[QP]  v w_q / 2                    (interactions: W_q = h_q P_q)
 //   per element s:
 //     rho[QP]   = B_sq / A_sq           (EXTEND of an o = 0 element)
-//     C[QP]     = v w_q (1 - z_s)/A_sq  (SHAP: phi_s = sum_q P_q C_sq when o_s = 1)
+//     C'[QP]    = v w_q ((1 - z_s)/A_sq + 1/(1 - t_q))   (SHAP: C_sq - d_q, where
+//               C_sq = v w_q (1-z_s)/A_sq gives phi_s = sum_q P_q C_sq when o_s = 1)
 //     alpha[QP] = (1 - z_s) / A_sq      (interactions: u_sq when o_s = 1)
 GTS_HD constexpr int nodal_qp(int q) { return (q + 3) & ~3; }
 GTS_HD constexpr int nodal_path_words(int k, int q) { return 3 * nodal_qp(q) * (k + 1); }

@@ -765,9 +765,9 @@ static void write_regions(const NodalPlan& np, int S, char* out) {
       int32_t lo, hi;
       std::memcpy(&lo, &er.lo, 4);
       std::memcpy(&hi, &er.hi, 4);
-      E[4 * e + 0] = er.slot;
-      E[4 * e + 1] = lo;
-      E[4 * e + 2] = hi;
+      E[4 * e + 0] = lo;
+      E[4 * e + 1] = hi;
+      E[4 * e + 2] = er.slot;
       E[4 * e + 3] = er.slot * (2 * S - er.slot - 1) / 2;  // upper-triangle row base of the slot
     }
     for (int32_t p = 0; p < c.n_paths; ++p) {
@@ -792,7 +792,7 @@ static void write_regions(const NodalPlan& np, int S, char* out) {
           const long double A = z + (1.0L - z) * tt, B = z * (1.0L - tt);
           T* row = t + 3 * QP + s * 3 * QP;
           row[q] = (T)(B / A);
-          row[QP + q] = (T)(v * w * (1.0L - z) / A);
+          row[QP + q] = (T)(v * w * ((1.0L - z) / A + 1.0L / (1.0L - tt)));  // C' = C - d
           row[2 * QP + q] = (T)((1.0L - z) / A);
         }
       }

@@ -130,8 +130,22 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   per_sm = std::max(per_sm, 1);
   const int64_t row_tiles = (n_rows + W * 32 * R - 1) / (W * 32 * R);
-  const int64_t target = (int64_t)num_sms() * per_sm * 2;
+  const int64_t resident = (int64_t)num_sms() * per_sm;
+  const int64_t target = resident * 2;
   int64_t splits = (target + row_tiles - 1) / row_tiles;
+  {
+    // Blocks run in index order (row tile major, split minor), so the first
+    // `resident` blocks cover resident / splits row tiles.  Keep the rows in
+    // flight small enough that their X rows and one group's phi (phi_ij) rows
+    // stay in L2 (wide models: the chunk gathers re-read X and the flush REDs
+    // hit phi once per chunk); splits only add one flush per split boundary.
+    const int64_t M1 = info->n_features + 1;
+    const int64_t bytes_per_row = (int64_t)sizeof(T) * (info->n_features + (kInter ? M1 * M1 : M1));
+    const int64_t l2_budget = 32ll << 20;
+    const int64_t rows_per_block = (int64_t)W * 32 * R;
+    const int64_t want = (resident * rows_per_block * bytes_per_row + l2_budget - 1) / l2_budget;
+    splits = std::max(splits, std::min(want, row_tiles > 0 ? resident : 1));
+  }
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, std::min<int64_t>(info->n_units, 1024)));
   nodal::Args a;
   a.blob = d_blob;

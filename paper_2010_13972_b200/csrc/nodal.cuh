@@ -15,6 +15,7 @@
 // UNWIND(i) is the division by f_i, folded into per-element constants:
 //   phi_i = v (o_i - z_i) U_i = sum_q P_q C_iq        (o_i = 1)
 //         = sum_q P_q d_q  (same for every o_i = 0)
+// (the table stores C' = C - d, see shap_run)
 // Interactions (Eq. 3, conditioning only on path features):
 //   phi_ij = sum_q (v w_q P_q / 2) u_iq u_jq,  u = (o - z)/f,
 //   phi_ii = sum_q (v w_q P_q / 2) u_iq (2 - sum_j u_jq + u_iq)    (Eq. 6)
@@ -24,6 +25,16 @@
 // registers and reach the shared-memory phi tile once per run.
 #pragma once
 #include "blob_format.h"
+
+#ifndef GTS_X2
+#define GTS_X2 1  // fp32 SHAP runs on paired Gauss nodes (FFMA2 / FMUL2)
+#endif
+#ifndef GTS_INTER_R8
+#define GTS_INTER_R8 2  // rows per lane of the fp32 interaction kernel with 8 slots
+#endif
+#ifndef GTS_SHAP_R8
+#define GTS_SHAP_R8 4  // rows per lane of the fp32 SHAP kernel with 8 slots (measured: 4 > 2)
+#endif
 
 namespace gts {
 namespace nodal {
@@ -62,12 +73,17 @@ __device__ __forceinline__ void lds_vec(T (&dst)[N], const T* src) {
 template <typename T>
 __device__ __forceinline__ bool one_fraction(T x, int4 rec) {
   // o = [lower <= x < upper]  (half-open bounds, reading G1)
-  return (x >= (T)__int_as_float(rec.y)) & (x < (T)__int_as_float(rec.z));
+  return (x >= (T)__int_as_float(rec.x)) & (x < (T)__int_as_float(rec.y));
 }
 
 // --------------------------------------------------------------------- SHAP
 
 // A run of n_run paths with one feature set; k in {2Q-1, 2Q}; fully unrolled.
+// UNWIND is folded into the table as C'_sq = C_sq - d_q, so that
+//   phi_s = ph0 + o_s sum_q P_q C'_sq,   ph0 = sum_q P_q d_q,
+// i.e. an o_s = 1 element costs one predicated FMA chain straight into its
+// accumulator and an o_s = 0 element costs nothing; ph0 is summed once per
+// path into one register per row and added to every slot of the run at its end.
 template <typename T, int Q, int R>
 __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restrict__ E, const T* __restrict__ tab,
                                          const int (&xb)[R], const int (&ab)[R]) {
@@ -75,10 +91,12 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
   T* const sT = reinterpret_cast<T*>(g_smem);
   const int words = nodal_path_words(k, Q);
   int slot[KM];
-  T acc[R][KM], xv[R][KM];  // the run's slots and this lane's x values, loaded once per run
+  T acc[R][KM], xv[R][KM], ph0[R];  // the run's slots and this lane's x values, loaded once per run
+#pragma unroll
+  for (int r = 0; r < R; ++r) ph0[r] = (T)0;
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
-    slot[s] = (s < KM - 1 || s < k) ? E[s].x : 0;
+    slot[s] = (s < KM - 1 || s < k) ? E[s].z : 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = (T)0;
@@ -109,7 +127,7 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool o = one_fraction(xv[r][s], rec);
-          if (o) om[r] |= 1u << s;
+          om[r] |= (uint32_t)o << s;
           if (!o) {
 #pragma unroll
             for (int q = 0; q < Q; ++q) P[r][q] *= rho[q];  // EXTEND: f_s = B_s for o_s = 0
@@ -117,17 +135,13 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
         }
       }
     }
-    T ph0[R];
     {
       T d[Q];
       lds_vec(d, tp + QP);
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        T a = (T)0;
+      for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int q = 0; q < Q; ++q) a = fma(P[r][q], d[q], a);
-        ph0[r] = a;
-      }
+        for (int q = 0; q < Q; ++q) ph0[r] = fma(P[r][q], d[q], ph0[r]);
     }
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
@@ -136,10 +150,10 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
         lds_vec(C, tp + 3 * QP + s * 3 * QP + QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          T a = (T)0;
+          if ((om[r] >> s) & 1u) {
 #pragma unroll
-          for (int q = 0; q < Q; ++q) a = fma(P[r][q], C[q], a);  // UNWIND(s) folded into C
-          acc[r][s] += ((om[r] >> s) & 1u) ? a : ph0[r];
+            for (int q = 0; q < Q; ++q) acc[r][s] = fma(P[r][q], C[q], acc[r][s]);  // UNWIND(s) folded into C'
+          }
         }
       }
     }
@@ -148,7 +162,98 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
   for (int s = 0; s < KM; ++s)
     if (s < KM - 1 || s < k)
 #pragma unroll
-      for (int r = 0; r < R; ++r) sT[ab[r] + slot[s]] += acc[r][s];
+      for (int r = 0; r < R; ++r) sT[ab[r] + slot[s]] += acc[r][s] + ph0[r];
+}
+
+// fp32 variant of shap_run on packed pairs of Gauss nodes: {P_q, P_q+1} live
+// in one 64-bit register pair and EXTEND / UNWIND use the sm_100 paired FP32
+// instructions (FMUL2 / FFMA2: one issue slot for two lanes' worth of FMA-pipe
+// work), predicated per row as before.  Pads (q >= Q) are zero in the table,
+// so P_pad = 0 and they contribute nothing.  acc keeps even/odd node partial
+// sums, folded once per run.
+template <int Q, int R>
+__device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __restrict__ E,
+                                            const float* __restrict__ tab, const int (&xb)[R], const int (&ab)[R]) {
+  constexpr int QP = QP_<Q>::v, KM = 2 * Q, QH = (Q + 1) / 2;
+  float* const sT = reinterpret_cast<float*>(g_smem);
+  const int words = nodal_path_words(k, Q);
+  int slot[KM];
+  float xv[R][KM];
+  float2 acc[R][KM], ph0[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) ph0[r] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int s = 0; s < KM; ++s) {
+    slot[s] = (s < KM - 1 || s < k) ? E[s].z : 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      acc[r][s] = make_float2(0.f, 0.f);
+      xv[r][s] = sT[xb[r] + slot[s]];
+    }
+  }
+  for (int p = 0; p < n_run; ++p) {
+    const int4* Ep = E + p * k;
+    const float2* tp = reinterpret_cast<const float2*>(tab + p * words);
+    float2 P[R][QH];
+#pragma unroll
+    for (int h = 0; h < QH; ++h) {
+      const float2 c = tp[h];
+#pragma unroll
+      for (int r = 0; r < R; ++r) P[r][h] = c;
+    }
+    uint32_t om[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) om[r] = 0u;
+#pragma unroll
+    for (int s = 0; s < KM; ++s) {
+      if (s < KM - 1 || s < k) {
+        const int4 rec = Ep[s];
+        const float2* rho = tp + (3 * QP + s * 3 * QP) / 2;
+        float2 rh[QH];
+#pragma unroll
+        for (int h = 0; h < QH; ++h) rh[h] = rho[h];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const bool o = one_fraction(xv[r][s], rec);
+          om[r] |= (uint32_t)o << s;
+          if (!o) {
+#pragma unroll
+            for (int h = 0; h < QH; ++h) P[r][h] = __fmul2_rn(P[r][h], rh[h]);  // EXTEND, f_s = B_s
+          }
+        }
+      }
+    }
+    {
+      const float2* d = tp + QP / 2;
+#pragma unroll
+      for (int h = 0; h < QH; ++h) {
+        const float2 dh = d[h];
+#pragma unroll
+        for (int r = 0; r < R; ++r) ph0[r] = __ffma2_rn(P[r][h], dh, ph0[r]);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < KM; ++s) {
+      if (s < KM - 1 || s < k) {
+        const float2* C = tp + (3 * QP + s * 3 * QP + QP) / 2;
+        float2 Ch[QH];
+#pragma unroll
+        for (int h = 0; h < QH; ++h) Ch[h] = C[h];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if ((om[r] >> s) & 1u) {
+#pragma unroll
+            for (int h = 0; h < QH; ++h) acc[r][s] = __ffma2_rn(P[r][h], Ch[h], acc[r][s]);  // UNWIND via C'
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < KM; ++s)
+    if (s < KM - 1 || s < k)
+#pragma unroll
+      for (int r = 0; r < R; ++r) sT[ab[r] + slot[s]] += (acc[r][s].x + acc[r][s].y) + (ph0[r].x + ph0[r].y);
 }
 
 // One path, element loop not unrolled (large Q); accumulates per element.
@@ -176,7 +281,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
     lds_vec(rho, tab + 3 * QP + s * 3 * QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool o = one_fraction(sT[xb[r] + rec.x], rec);
+      const bool o = one_fraction(sT[xb[r] + rec.z], rec);
       om[r] |= (uint32_t)o << s;
       if (!o) {
 #pragma unroll
@@ -198,15 +303,17 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
   }
 #pragma unroll 1
   for (int s = 0; s < k; ++s) {
-    const int sl = E[s].x;
+    const int sl = E[s].z;
     T C[Q];
     lds_vec(C, tab + 3 * QP + s * 3 * QP + QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      T a = (T)0;
+      T a = ph0[r];
+      if ((om[r] >> s) & 1u) {
 #pragma unroll
-      for (int q = 0; q < Q; ++q) a = fma(P[r][q], C[q], a);
-      sT[ab[r] + sl] += ((om[r] >> s) & 1u) ? a : ph0[r];
+        for (int q = 0; q < Q; ++q) a = fma(P[r][q], C[q], a);
+      }
+      sT[ab[r] + sl] += a;
     }
   }
 }
@@ -235,7 +342,7 @@ __device__ __forceinline__ void inter_extend(int k, const int4* __restrict__ E, 
     lds_vec(rho, tp + 3 * QP + s * 3 * QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool o = one_fraction(sT[xb[r] + rec.x], rec);
+      const bool o = one_fraction(sT[xb[r] + rec.z], rec);
       om[r] |= (uint32_t)o << s;
       if (!o) {
 #pragma unroll
@@ -273,10 +380,10 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
   for (int s = 0; s < KM; ++s) {
     const bool valid = (s < KM - 1 || s < k);
     const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
-    slot[s] = e.x;
+    slot[s] = e.z;
     rb[s] = e.w;
 #pragma unroll
-    for (int r = 0; r < R; ++r) xv[r][s] = sT[xb[r] + e.x];
+    for (int r = 0; r < R; ++r) xv[r][s] = sT[xb[r] + e.z];
   }
   T acc[R][kRegAcc ? NC : 1];
 #pragma unroll
@@ -354,9 +461,10 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
         T y[R][Q], phi[R], yg[R];
         T ai[Q];
         if constexpr (!kCacheU) lds_vec(ai, tp + 3 * QP + i * 3 * QP + 2 * QP);
+        const int cdiag = c++;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          T a = (T)0, g = (T)0;
+          T a = kRegAcc ? acc[r][cdiag] : (T)0, g = (T)0;
           const bool oi = (om[r] >> i) & 1u;
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
@@ -364,13 +472,12 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
             if constexpr (kCacheU) ui = u[r][i][q];
             else ui = oi ? ai[q] : G[q];
             y[r][q] = W[r][q] * ui;
-            a += y[r][q];
+            a = fma(y[r][q], (T)2, a);  // phi_i = 2 sum_q W_q u_iq
             if constexpr (!kCacheU) g = fma(y[r][q], G[q], g);
           }
-          phi[r] = a + a;  // phi_i
+          phi[r] = a;
           yg[r] = g;
         }
-        const int cdiag = c++;
 #pragma unroll
         for (int j = i + 1; j < KM; ++j) {
           if (j < KM - 1 || j < k) {
@@ -378,16 +485,29 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
             if constexpr (!kCacheU) lds_vec(aj, tp + 3 * QP + j * 3 * QP + 2 * QP);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-              T v = (T)0;
-              if constexpr (kCacheU) {
+              if constexpr (kRegAcc) {
+                // the pair's dot product accumulates straight into its register
+                if constexpr (kCacheU) {
 #pragma unroll
-                for (int q = 0; q < Q; ++q) v = fma(y[r][q], u[r][j][q], v);
+                  for (int q = 0; q < Q; ++q) acc[r][c] = fma(y[r][q], u[r][j][q], acc[r][c]);
+                } else if ((om[r] >> j) & 1u) {
+#pragma unroll
+                  for (int q = 0; q < Q; ++q) acc[r][c] = fma(y[r][q], aj[q], acc[r][c]);
+                } else {
+                  acc[r][c] += yg[r];
+                }
               } else {
+                T v = (T)0;
+                if constexpr (kCacheU) {
 #pragma unroll
-                for (int q = 0; q < Q; ++q) v = fma(y[r][q], aj[q], v);
-                v = ((om[r] >> j) & 1u) ? v : yg[r];
+                  for (int q = 0; q < Q; ++q) v = fma(y[r][q], u[r][j][q], v);
+                } else {
+#pragma unroll
+                  for (int q = 0; q < Q; ++q) v = fma(y[r][q], aj[q], v);
+                  v = ((om[r] >> j) & 1u) ? v : yg[r];
+                }
+                add(r, c, i, j, v);
               }
-              add(r, c, i, j, v);
             }
           }
           ++c;
@@ -395,7 +515,10 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
         // the diagonal cell collects phi_i; Eq. 6 subtracts the row sums when
         // the tile is flushed (linear in the paths, so it holds per tile)
 #pragma unroll
-        for (int r = 0; r < R; ++r) add(r, cdiag, i, i, phi[r]);
+        for (int r = 0; r < R; ++r) {
+          if constexpr (kRegAcc) acc[r][cdiag] = phi[r];
+          else add(r, cdiag, i, i, phi[r]);
+        }
       } else {
         c += KM - i;
       }
@@ -454,11 +577,11 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
         g = fma(y[r][q], G[q], g);
       }
       yg[r] = g;
-      sT[ab[r] + ri.w + ri.x] += phi + phi;  // phi_i; Eq. 6 applied at flush
+      sT[ab[r] + ri.w + ri.z] += phi + phi;  // phi_i; Eq. 6 applied at flush
     }
 #pragma unroll 1
     for (int j = i + 1; j < k; ++j) {
-      const int cell = ri.w + E[j].x;
+      const int cell = ri.w + E[j].z;
       T aj[Q];
       lds_vec(aj, tp + 3 * QP + j * 3 * QP + 2 * QP);
 #pragma unroll
@@ -484,7 +607,34 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
   const int4* E = E0 + ph.z;
   const T* tab = table + ph.w;
   const int words = nodal_path_words(k, q);
-  if constexpr (!kInter) {
+  if constexpr (!kInter && GTS_X2 && sizeof(T) == 4 && R <= 2) {
+    // fp32: paired-node FFMA2 runs (Q >= 2); Q = 1 has nothing to pair
+    switch (q) {
+      case 1: shap_run<T, 1, R>(k, n_run, E, tab, xb, ab); break;
+#define GTS_RUN(QQ) case QQ: shap_run_x2<QQ, R>(k, n_run, E, reinterpret_cast<const float*>(tab), xb, ab); break;
+      GTS_RUN(2) GTS_RUN(3) GTS_RUN(4)
+#undef GTS_RUN
+      default:
+#pragma unroll 1
+        for (int r = 0; r < R; ++r) {
+          const int xb1[1] = {xb[r]}, ab1[1] = {ab[r]};
+          switch (q) {
+#define GTS_RUN1(QQ) case QQ: shap_run_x2<QQ, 1>(k, n_run, E, reinterpret_cast<const float*>(tab), xb1, ab1); break;
+            GTS_RUN1(5) GTS_RUN1(6) GTS_RUN1(7) GTS_RUN1(8)
+#undef GTS_RUN1
+            default:
+              for (int p = 0; p < n_run; ++p) {
+                switch (q) {
+#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1>(k, E + p * k, tab + p * words, xb1, ab1); break;
+                  GTS_DYN(9) GTS_DYN(10) GTS_DYN(11) GTS_DYN(12) GTS_DYN(13) GTS_DYN(14) GTS_DYN(15) GTS_DYN(16)
+#undef GTS_DYN
+                  default: break;
+                }
+              }
+          }
+        }
+    }
+  } else if constexpr (!kInter) {
     switch (q) {
 #define GTS_RUN(QQ) case QQ: shap_run<T, QQ, R>(k, n_run, E, tab, xb, ab); break;
       GTS_RUN(1) GTS_RUN(2) GTS_RUN(3) GTS_RUN(4)
@@ -572,7 +722,9 @@ __host__ __device__ constexpr int tile_words_per_warp() {
 // per block, chosen so that two blocks (tiles + chunk staging) share an SM.
 template <typename T, bool kInter, int S>
 struct Cfg {
-  static constexpr int R = (sizeof(T) == 4 && (kInter ? S <= 8 : S <= 16)) ? 2 : 1;
+  static constexpr int R = (sizeof(T) == 4 && !kInter && S == 8) ? GTS_SHAP_R8
+                           : (sizeof(T) == 4 && kInter && S == 8) ? GTS_INTER_R8
+                           : ((sizeof(T) == 4 && !kInter && S <= 16) ? 2 : 1);
   static constexpr int tile_bytes = (int)sizeof(T) * tile_words_per_warp<T, S, R, kInter>();
   static constexpr int W = tile_bytes * 8 <= 74 * 1024 ? 8 : (tile_bytes * 4 <= 80 * 1024 ? 4 : 2);
   static constexpr int kMinBlocks = 2;
@@ -691,41 +843,53 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
   auto flush = [&]() {
     if (dirty) {
       __syncwarp();
-      const int total = ROWS * cur_slots;  // (row, slot) pairs, slot fastest
-      for (int idx = lane; idx < total; idx += 32) {
-        const int rr = idx / cur_slots, i = idx - rr * cur_slots;
-        const int fi = slotmap[cur_map_begin + i];
-        {
+      if constexpr (kInter) {
+        const int total = ROWS * cur_slots;  // (row, slot) pairs, slot fastest
+        for (int idx = lane; idx < total; idx += 32) {
+          const int rr = idx / cur_slots, i = idx - rr * cur_slots;
+          const int fi = slotmap[cur_map_begin + i];
           const int64_t rg = row0 + rr;
-          T* tile = sT + o_acc + (tile_row0 + rr) * AS;
-          if constexpr (kInter) {
-            const int rbi = tri_row_base(i, S);
-            if (rg < a.n_rows) {
-              T* base = out + ((size_t)rg * a.G + cur_group) * (size_t)M1 * M1;
-              // the diagonal cell holds sum phi_i; Eq. 6: phi_ii = phi_i - sum_{j != i} phi_ij
-              T rowsum = (T)0;
-              for (int j = 0; j < cur_slots; ++j)
-                if (j != i) rowsum += tile[j < i ? tri_row_base(j, S) + i : rbi + j];
-              const T d = tile[rbi + i] - rowsum;
-              if (d != (T)0) atomicAdd(base + (size_t)fi * M1 + fi, d);
-              for (int j = i + 1; j < cur_slots; ++j) {
-                const T v = tile[rbi + j];
-                if (v != (T)0) {
-                  const int fj = slotmap[cur_map_begin + j];
-                  atomicAdd(base + (size_t)fi * M1 + fj, v);
-                  atomicAdd(base + (size_t)fj * M1 + fi, v);
-                }
+          const T* tile = sT + o_acc + (tile_row0 + rr) * AS;
+          const int rbi = tri_row_base(i, S);
+          if (rg < a.n_rows) {
+            T* base = out + ((size_t)rg * a.G + cur_group) * (size_t)M1 * M1;
+            // the diagonal cell holds sum phi_i; Eq. 6: phi_ii = phi_i - sum_{j != i} phi_ij
+            T rowsum = (T)0;
+            for (int j = 0; j < cur_slots; ++j)
+              if (j != i) rowsum += tile[j < i ? tri_row_base(j, S) + i : rbi + j];
+            const T d = tile[rbi + i] - rowsum;
+            if (d != (T)0) atomicAdd(base + (size_t)fi * M1 + fi, d);
+            for (int j = i + 1; j < cur_slots; ++j) {
+              const T v = tile[rbi + j];
+              if (v != (T)0) {
+                const int fj = slotmap[cur_map_begin + j];
+                atomicAdd(base + (size_t)fi * M1 + fj, v);
+                atomicAdd(base + (size_t)fj * M1 + fi, v);
               }
             }
-          } else {
-            const T v = tile[i];
-            if (rg < a.n_rows && v != (T)0) atomicAdd(out + ((size_t)rg * a.G + cur_group) * (size_t)M1 + fi, v);
+          }
+        }
+        __syncwarp();
+        // zero the tiles (interaction rows are read across lanes above, so only now)
+        for (int rr = 0; rr < ROWS; ++rr)
+          for (int c = lane; c < AW; c += 32) sT[o_acc + (tile_row0 + rr) * AS + c] = (T)0;
+      } else {
+        // lane = slot, rows walked in order: consecutive lanes hit consecutive
+        // features of one row (coalesced RED); each lane zeroes the cells it read
+        const size_t rstride = (size_t)a.G * M1;
+        const int64_t nr = a.n_rows - row0;
+        for (int i = lane; i < cur_slots; i += 32) {
+          const int fi = slotmap[cur_map_begin + i];
+          T* col = sT + o_acc + tile_row0 * AS + i;
+          T* dst = out + ((size_t)row0 * a.G + cur_group) * (size_t)M1 + fi;
+#pragma unroll 4
+          for (int rr = 0; rr < ROWS; ++rr) {
+            const T v = col[rr * AS];
+            col[rr * AS] = (T)0;
+            if (rr < nr && v != (T)0) atomicAdd(dst + rr * rstride, v);
           }
         }
       }
-      __syncwarp();
-      // zero the tiles (interaction rows are read across lanes above, so only now)
-      for (int idx = lane; idx < ROWS * AW; idx += 32) sT[o_acc + (tile_row0 + idx / AW) * AS + idx % AW] = (T)0;
       __syncwarp();
     }
     dirty = false;

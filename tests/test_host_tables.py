@@ -163,15 +163,15 @@ def test_nodal_blob_invariants(name, slots):
             run = P[i, 0] >> 16
             assert run >= 1
             k = P[i, 0] & 0xFF
-            feats0 = tuple(mp[E[P[i, 2]:P[i, 2] + k, 0]])
+            feats0 = tuple(mp[E[P[i, 2]:P[i, 2] + k, 2]])
             for j in range(run):
                 kk, Q, e0, t0 = P[i + j, 0] & 0xFF, P[i + j, 1], P[i + j, 2], P[i + j, 3]
                 QP = (Q + 3) & ~3
                 assert kk == k and Q == (k + 1) // 2
                 el = E[e0:e0 + k]
-                feats = tuple(mp[el[:, 0]])
+                feats = tuple(mp[el[:, 2]])
                 assert feats == feats0
-                np.testing.assert_array_equal(el[:, 3], el[:, 0] * (2 * hd["S"] - el[:, 0] - 1) // 2)
+                np.testing.assert_array_equal(el[:, 3], el[:, 2] * (2 * hd["S"] - el[:, 2] - 1) // 2)
                 t, wq = g[Q - 1, 0, :Q], g[Q - 1, 1, :Q]
                 h = tab[t0 + 2 * QP:t0 + 2 * QP + Q]
                 v = float(2 * h[0] / wq[0])
@@ -185,9 +185,11 @@ def test_nodal_blob_invariants(name, slots):
                 np.testing.assert_allclose(h, 0.5 * v * wq, rtol=1e-12, atol=1e-300)
                 rows = tab[t0 + 3 * QP:t0 + 3 * QP * (k + 1)].reshape(k, 3, QP)[:, :, :Q]
                 np.testing.assert_allclose(rows[:, 0], B / A, rtol=1e-12)
-                np.testing.assert_allclose(rows[:, 1], v * wq[None] * (1 - z[:, None]) / A, rtol=1e-12, atol=1e-300)
+                # C' = C - d: the SHAP constant with the o = 0 share folded out (nodal.cuh shap_run)
+                np.testing.assert_allclose(rows[:, 1], v * wq[None] * ((1 - z[:, None]) / A + 1 / (1 - t[None])),
+                                           rtol=1e-12, atol=1e-300)
                 np.testing.assert_allclose(rows[:, 2], (1 - z[:, None]) / A, rtol=1e-12, atol=1e-300)
-                lo = E[e0:e0 + k, 1].view(np.float32)
+                lo = E[e0:e0 + k, 0].view(np.float32)
                 assert np.all(lo == lo)  # bounds stored as fp32 bit patterns
                 seen += 1
             i += run
