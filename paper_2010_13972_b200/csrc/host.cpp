@@ -512,6 +512,10 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
       if (tab.group[p] == g && tab.len(p) > 1) order.push_back(p);
     if (identity) std::sort(order.begin() + first, order.end(), fs_less);
   }
+  // (Cutting small models into ~one chunk per SM lowered the 1-row latency of
+  // cal_housing-small from 23 to 18 us but cost 30 % at 2^20 rows, since runs
+  // and staging get shorter; profiles/r01h.  Not adopted.)
+  const int chunk_paths = kMaxChunkPaths;
   // staged bytes of a chunk: element records + path headers (16 B each) + tables
   auto path_bytes = [&](int k, int q) { return (int64_t)16 * (k + 1) + (int64_t)tsize * nodal_path_words(k, q); };
   int32_t map_id = -1;
@@ -526,7 +530,7 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
     std::vector<int64_t> members;
     int64_t bytes = 0, nel = 0;
     size_t j = i;
-    while (j < order.size() && (int)members.size() < kMaxChunkPaths) {
+    while (j < order.size() && (int)members.size() < chunk_paths) {
       const int64_t p = order[j];
       if (tab.group[p] != c.group) break;
       const int k = tab.len(p) - 1, q = (k + 1) / 2;

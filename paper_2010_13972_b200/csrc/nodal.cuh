@@ -30,7 +30,16 @@
 #define GTS_X2 1  // fp32 SHAP runs on paired Gauss nodes (FFMA2 / FMUL2)
 #endif
 #ifndef GTS_INTER_R8
-#define GTS_INTER_R8 2  // rows per lane of the fp32 interaction kernel with 8 slots
+#define GTS_INTER_R8 1  // rows per lane of the fp32 interaction kernel with 8 slots
+                        // (measured: 1 row, 8 warps per block beats 2 rows, 4 warps by 8 %; profiles/r01h)
+#endif
+#ifndef GTS_INTER_Q2
+#define GTS_INTER_Q2 2  // fp32 interaction runs on paired Gauss nodes: 1 = Q 3 and 4, 2 = Q 4 only
+                        // (measured: 2 is best, +3 % cal_housing, +10 % adult; profiles/r01i)
+#endif
+#ifndef GTS_X2_R2_QMAX
+#define GTS_X2_R2_QMAX 6  // largest Q whose paired-node SHAP run keeps both rows of a lane in flight
+                          // (measured: adult SHAP +19 % for 6 over 4; profiles/r01h)
 #endif
 #ifndef GTS_SHAP_R8
 #define GTS_SHAP_R8 4  // rows per lane of the fp32 SHAP kernel with 8 slots (measured: 4 > 2)
@@ -437,7 +446,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
     }
     // u_s = (o_s - z_s)/f_s(t_q): cached in registers for small paths; for
     // larger ones the partner's u is applied as a select on the dot product
-    constexpr bool kCacheU = Q <= 5;
+    constexpr bool kCacheU = Q <= 4;  // Q = 5 would put u in local memory
     T u[R][kCacheU ? KM : 1][Q];
     if constexpr (kCacheU) {
 #pragma unroll
@@ -539,6 +548,106 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
   }
 }
 
+// fp32, one row: inter_run on packed pairs of Gauss nodes.  Every cell keeps
+// an {even node, odd node} partial sum, so the pair products, the diagonal
+// sums, W and y run on paired FP32 instructions (FFMA2 / FMUL2) and the run's
+// cells stay in registers even for Q = 4 (where the scalar version writes each
+// pair to the shared tile).  Pads q >= Q are zero in the table (P_pad = 0).
+template <int Q>
+__device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __restrict__ E,
+                                             const float* __restrict__ tab, const float* __restrict__ gam,
+                                             const int (&xb)[1], const int (&ab)[1]) {
+  constexpr int QP = QP_<Q>::v, KM = 2 * Q, NC = KM * (KM + 1) / 2, QH = (Q + 1) / 2;
+  float* const sT = reinterpret_cast<float*>(g_smem);
+  const int words = nodal_path_words(k, Q);
+  float2 G[QH];
+#pragma unroll
+  for (int h = 0; h < QH; ++h) G[h] = make_float2(gam[2 * h], 2 * h + 1 < Q ? gam[2 * h + 1] : 0.f);
+  int slot[KM], rb[KM];
+  float xv[KM];
+#pragma unroll
+  for (int s = 0; s < KM; ++s) {
+    const bool valid = (s < KM - 1 || s < k);
+    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
+    slot[s] = e.z;
+    rb[s] = e.w;
+    xv[s] = sT[xb[0] + e.z];
+  }
+  float2 acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = make_float2(0.f, 0.f);
+  for (int p = 0; p < n_run; ++p) {
+    const int4* Ep = E + p * k;
+    const float2* tp = reinterpret_cast<const float2*>(tab + p * words);
+    float2 P[QH];
+#pragma unroll
+    for (int h = 0; h < QH; ++h) P[h] = tp[h];
+    uint32_t om = 0u;
+#pragma unroll
+    for (int s = 0; s < KM; ++s) {
+      if (s < KM - 1 || s < k) {
+        const bool o = one_fraction(xv[s], Ep[s]);
+        om |= (uint32_t)o << s;
+        if (!o) {
+          const float2* rho = tp + (3 * QP + s * 3 * QP) / 2;
+#pragma unroll
+          for (int h = 0; h < QH; ++h) P[h] = __fmul2_rn(P[h], rho[h]);  // EXTEND at the nodes
+        }
+      }
+    }
+    float2 W[QH];
+#pragma unroll
+    for (int h = 0; h < QH; ++h) W[h] = __fmul2_rn(P[h], tp[QP + h]);  // h_q = v w_q / 2
+    float2 u[KM][QH];
+#pragma unroll
+    for (int s = 0; s < KM; ++s) {
+      if (s < KM - 1 || s < k) {
+        const float2* al = tp + (3 * QP + s * 3 * QP + 2 * QP) / 2;
+        const bool o = (om >> s) & 1u;
+#pragma unroll
+        for (int h = 0; h < QH; ++h) {
+          const float2 a = al[h];
+          u[s][h] = make_float2(o ? a.x : G[h].x, o ? a.y : G[h].y);  // UNWIND(s) folded into u
+        }
+      }
+    }
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < KM; ++i) {
+      if (i < KM - 1 || i < k) {
+        float2 y[QH];
+        const int cdiag = c++;
+        float2 a = acc[cdiag];
+#pragma unroll
+        for (int h = 0; h < QH; ++h) {
+          y[h] = __fmul2_rn(W[h], u[i][h]);
+          a = __ffma2_rn(y[h], make_float2(2.f, 2.f), a);  // phi_i = 2 sum_q W_q u_iq
+        }
+#pragma unroll
+        for (int j = i + 1; j < KM; ++j) {
+          if (j < KM - 1 || j < k) {
+#pragma unroll
+            for (int h = 0; h < QH; ++h) acc[c] = __ffma2_rn(y[h], u[j][h], acc[c]);
+          }
+          ++c;
+        }
+        acc[cdiag] = a;  // Eq. 6 subtracts the row sums when the tile is flushed
+      } else {
+        c += KM - i;
+      }
+    }
+  }
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < KM; ++i) {
+#pragma unroll
+    for (int j = i; j < KM; ++j) {
+      if ((i < KM - 1 || i < k) && (j < KM - 1 || j < k)) sT[ab[0] + rb[i] + slot[j]] += acc[c].x + acc[c].y;
+      ++c;
+    }
+  }
+}
+
 // One path, pair cells accumulated straight into the shared tile.
 template <typename T, int Q, int R, bool kUnroll>
 __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, const T* __restrict__ tp,
@@ -613,6 +722,12 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
       case 1: shap_run<T, 1, R>(k, n_run, E, tab, xb, ab); break;
 #define GTS_RUN(QQ) case QQ: shap_run_x2<QQ, R>(k, n_run, E, reinterpret_cast<const float*>(tab), xb, ab); break;
       GTS_RUN(2) GTS_RUN(3) GTS_RUN(4)
+#if GTS_X2_R2_QMAX >= 5
+      GTS_RUN(5)
+#endif
+#if GTS_X2_R2_QMAX >= 6
+      GTS_RUN(6)
+#endif
 #undef GTS_RUN
       default:
 #pragma unroll 1
@@ -669,8 +784,22 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
         for (int r = 0; r < R; ++r) {
           const int xb1[1] = {xb[r]}, ab1[1] = {ab[r]};
           switch (q) {
-            case 3: inter_run<T, 3, 1, true>(k, n_run, E, tab, gam, xb1, ab1); break;
-            case 4: inter_run<T, 4, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break;
+            case 3:
+              if constexpr (GTS_INTER_Q2 == 1 && sizeof(T) == 4) {
+                inter_run_q2<3>(k, n_run, E, reinterpret_cast<const float*>(tab),
+                                reinterpret_cast<const float*>(gam), xb1, ab1);
+              } else {
+                inter_run<T, 3, 1, true>(k, n_run, E, tab, gam, xb1, ab1);
+              }
+              break;
+            case 4:
+              if constexpr (GTS_INTER_Q2 && sizeof(T) == 4) {
+                inter_run_q2<4>(k, n_run, E, reinterpret_cast<const float*>(tab),
+                                reinterpret_cast<const float*>(gam), xb1, ab1);
+              } else {
+                inter_run<T, 4, 1, false>(k, n_run, E, tab, gam, xb1, ab1);
+              }
+              break;
             case 5: inter_run<T, 5, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break;
             case 6:
               if constexpr (sizeof(T) == 4) { inter_run<T, 6, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break; }

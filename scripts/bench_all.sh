@@ -6,6 +6,7 @@ mkdir -p $OUT
 run() { local name=$1; shift; timeout 1200 python bench.py --workload "$@" > $OUT/$name.json 2> $OUT/$name.err; echo "$name rc=$?"; }
 run cal_housing-small cal_housing-small --rows-per-gpu 1048576 --steps 10 --no-ablation ${EXTRA:-}
 run cal_housing-med cal_housing-med --rows-per-gpu 1048576 --steps 10 ${EXTRA:-}
+run cal_housing-med-f64 cal_housing-med --rows-per-gpu 262144 --steps 5 --dtype f64 --no-ablation ${EXTRA:-}
 run adult-large adult-large --rows-per-gpu 65536 --steps 5 ${EXTRA:-}
 run fashion_mnist-med fashion_mnist-med --rows-per-gpu 65536 --steps 5 --mode shap --x-layout feature ${EXTRA:-}
 run fashion_mnist-med-rowmajor fashion_mnist-med --rows-per-gpu 65536 --steps 5 --mode shap --no-ablation ${EXTRA:-}

@@ -22,6 +22,9 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
      python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-ablation ${BENCH_ARGS:-} > $OUT/ncu_launch.log 2>&1
   echo "ncu launches rc=$?"
-  OUT=$OUT NAME=${NAME:-nodal_full} WL=${WL:-cal_housing-med} ROWS=${NCU_ROWS:-1048576} MODE=both KEEP=${KEEP:-0} bash scripts/ncu_one.sh
-  cat $OUT/${NAME:-nodal_full}.summary.txt | head -80
+  # one capture per kernel (a long second kernel in the same process came back as nan twice)
+  for m in shap interactions; do
+    OUT=$OUT NAME=nodal_$m WL=${WL:-cal_housing-med} ROWS=${NCU_ROWS:-1048576} MODE=$m KEEP=${KEEP:-0} bash scripts/ncu_one.sh
+    head -24 $OUT/nodal_$m.summary.txt
+  done
 fi

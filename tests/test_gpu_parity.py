@@ -271,3 +271,33 @@ def test_graphed_call_small_batches(gpu, inter):
             got = g.replay().cpu().numpy()
             ref = (oracle.interactions if inter else oracle.treeshap)(ens, x.astype(np.float64))
             parity.check(got, ref, "f32", f"graphed n={n} inter={inter}")
+
+
+def test_row_shards_and_replicated_blob(gpu):
+    """a9: rows sharded over 4 'ranks' on one device, each with
+    its own copy of the blob bytes (what the NCCL broadcast delivers), give
+    the single-call result; rows on both sides of every shard boundary are
+    checked against the oracle."""
+    import torch
+    from paper_2010_13972_b200.explainer import Blob
+    w = WORKLOADS["adult-large"]
+    ens = w.ensemble().subset(range(200))
+    n, N = 4099, 4
+    x = w.x(n, ens=ens)
+    ex = _explainer(ens, "f32", "nodal")
+    xd = torch.from_numpy(x).cuda()
+    full = ex.shap_device(xd).cpu().numpy()
+    cuts = [r * n // N for r in range(N + 1)]
+    parts = []
+    for r in range(N):
+        rep = Blob(ex.blob.info, ex.blob.data.clone())
+        out = torch.empty((cuts[r + 1] - cuts[r], 1, w.n_features + 1), device="cuda")
+        from paper_2010_13972_b200 import gts
+        xs = xd[cuts[r]:cuts[r + 1]]
+        gts.gts_shap(rep.info, rep.ptr, xs.data_ptr(), xs.shape[0], w.n_features, out.data_ptr(),
+                     torch.cuda.current_stream().cuda_stream)
+        parts.append(out.cpu().numpy())
+    cat = np.concatenate(parts)
+    parity.check(cat, full.astype(np.float64), "f32", "shards vs single call")
+    edge = sorted({c for b in cuts[1:-1] for c in (b - 1, b)})
+    parity.check(cat[edge], oracle.treeshap(ens, x[edge].astype(np.float64)), "f32", "shard boundaries")
