@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define GTS_ABI_VERSION 1
+#define GTS_ABI_VERSION 2  /* 2: blob element records {lo, hi, slot, tri}, C' tables, 2-table blobs above 16 slots */
 #define GTS_WARP_CAPACITY 32 /* lanes per warp = bin capacity B */
 
 typedef enum gts_status {

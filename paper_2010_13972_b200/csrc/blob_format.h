@@ -80,7 +80,8 @@ struct ElemRec {
   double z;                    // merged zero fraction
 };
 
-// Nodal table of one path (T words, shared memory).  Every row is padded to
+// Nodal table of one path (T words, shared memory; NT = nodal_tables(S) rows
+// per record, the third row only when NT = 3).  Every row is padded to
 // QP = round_up(Q, 4) words (16-byte vector loads).  With A_sq = z_s + (1-z_s) t_q,
 // B_sq = z_s (1 - t_q) (f_s(t_q) for o_s = 1 / 0):
 //   c[QP]  prod_s A_sq                  (P(t_q) when every o = 1)
@@ -92,7 +93,12 @@ struct ElemRec {
 //               C_sq = v w_q (1-z_s)/A_sq gives phi_s = sum_q P_q C_sq when o_s = 1)
 //     alpha[QP] = (1 - z_s) / A_sq      (interactions: u_sq when o_s = 1)
 GTS_HD constexpr int nodal_qp(int q) { return (q + 3) & ~3; }
-GTS_HD constexpr int nodal_path_words(int k, int q) { return 3 * nodal_qp(q) * (k + 1); }
+// Blobs with more than 16 slots serve only the SHAP kernel (the interaction
+// kernel takes 8 or 16 slots), so they drop h and alpha: NT = 2 tables per
+// row ({c, d} and {rho, C'} per element) instead of 3 -- 1.5x more paths per
+// 16 KB chunk, hence fewer slot-map gathers and flushes for wide models.
+GTS_HD constexpr int nodal_tables(int slots) { return slots > 16 ? 2 : 3; }
+GTS_HD constexpr int nodal_path_words(int k, int q, int nt = 3) { return nt * nodal_qp(q) * (k + 1); }
 
 // WARP_BINS lane arrays (each [n_bins * 32], in this order after off_elems):
 //   int32 feature   (-1 root lane, -2 empty lane)

@@ -517,7 +517,8 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
   // and staging get shorter; profiles/r01h.  Not adopted.)
   const int chunk_paths = kMaxChunkPaths;
   // staged bytes of a chunk: element records + path headers (16 B each) + tables
-  auto path_bytes = [&](int k, int q) { return (int64_t)16 * (k + 1) + (int64_t)tsize * nodal_path_words(k, q); };
+  const int nt = nodal_tables(S);
+  auto path_bytes = [&](int k, int q) { return (int64_t)16 * (k + 1) + (int64_t)tsize * nodal_path_words(k, q, nt); };
   int32_t map_id = -1;
   std::vector<int32_t> cur_map;  // sorted features of the current chunk (non-identity)
   size_t i = 0;
@@ -594,7 +595,7 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
         np.elems.push_back(er);
       }
       rel += k;
-      table += nodal_path_words(k, q);
+      table += nodal_path_words(k, q, nt);
       maxq = std::max(maxq, q);
       ws += nodal_shap_flops(k, q);
       wi += nodal_inter_flops(k, q);
@@ -756,6 +757,7 @@ template <typename T>
 static void write_regions(const NodalPlan& np, int S, char* out) {
   long double tq[kQMax + 1][kQMax], wq[kQMax + 1][kQMax];
   for (int Q = 1; Q <= kQMax; ++Q) gauss_legendre01(Q, tq[Q], wq[Q]);
+  const int nt = nodal_tables(S);
   const int64_t C = (int64_t)np.chunks.size();
 #pragma omp parallel for schedule(dynamic, 16)
   for (int64_t ci = 0; ci < C; ++ci) {
@@ -790,14 +792,14 @@ static void write_regions(const NodalPlan& np, int S, char* out) {
         for (int s = 0; s < k; ++s) cq *= (long double)el[s].z + (1.0L - el[s].z) * tt;
         t[q] = (T)cq;
         t[QP + q] = (T)(-v * w / (1.0L - tt));
-        t[2 * QP + q] = (T)(0.5L * v * w);
+        if (nt == 3) t[2 * QP + q] = (T)(0.5L * v * w);
         for (int s = 0; s < k; ++s) {
           const long double z = el[s].z;
           const long double A = z + (1.0L - z) * tt, B = z * (1.0L - tt);
-          T* row = t + 3 * QP + s * 3 * QP;
+          T* row = t + nt * QP + s * nt * QP;
           row[q] = (T)(B / A);
           row[QP + q] = (T)(v * w * ((1.0L - z) / A + 1.0L / (1.0L - tt)));  // C' = C - d
-          row[2 * QP + q] = (T)((1.0L - z) / A);
+          if (nt == 3) row[2 * QP + q] = (T)((1.0L - z) / A);
         }
       }
     }

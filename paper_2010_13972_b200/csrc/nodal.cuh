@@ -37,6 +37,9 @@
 #define GTS_INTER_Q2 2  // fp32 interaction runs on paired Gauss nodes: 1 = Q 3 and 4, 2 = Q 4 only
                         // (measured: 2 is best, +3 % cal_housing, +10 % adult; profiles/r01i)
 #endif
+#ifndef GTS_INTER_LEAN
+#define GTS_INTER_LEAN 0  // register-resident interaction runs re-read x / slots from shared (A/B knob)
+#endif
 #ifndef GTS_X2_R2_QMAX
 #define GTS_X2_R2_QMAX 6  // largest Q whose paired-node SHAP run keeps both rows of a lane in flight
                           // (measured: adult SHAP +19 % for 6 over 4; profiles/r01h)
@@ -93,12 +96,12 @@ __device__ __forceinline__ bool one_fraction(T x, int4 rec) {
 // i.e. an o_s = 1 element costs one predicated FMA chain straight into its
 // accumulator and an o_s = 0 element costs nothing; ph0 is summed once per
 // path into one register per row and added to every slot of the run at its end.
-template <typename T, int Q, int R>
+template <typename T, int Q, int R, int NT>
 __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restrict__ E, const T* __restrict__ tab,
                                          const int (&xb)[R], const int (&ab)[R]) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q;
   T* const sT = reinterpret_cast<T*>(g_smem);
-  const int words = nodal_path_words(k, Q);
+  const int words = nodal_path_words(k, Q, NT);
   int slot[KM];
   T acc[R][KM], xv[R][KM], ph0[R];  // the run's slots and this lane's x values, loaded once per run
 #pragma unroll
@@ -132,7 +135,7 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
       if (s < KM - 1 || s < k) {
         const int4 rec = Ep[s];
         T rho[Q];
-        lds_vec(rho, tp + 3 * QP + s * 3 * QP);
+        lds_vec(rho, tp + NT * QP + s * NT * QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool o = one_fraction(xv[r][s], rec);
@@ -156,7 +159,7 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
         T C[Q];
-        lds_vec(C, tp + 3 * QP + s * 3 * QP + QP);
+        lds_vec(C, tp + NT * QP + s * NT * QP + QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if ((om[r] >> s) & 1u) {
@@ -180,12 +183,12 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 // work), predicated per row as before.  Pads (q >= Q) are zero in the table,
 // so P_pad = 0 and they contribute nothing.  acc keeps even/odd node partial
 // sums, folded once per run.
-template <int Q, int R>
+template <int Q, int R, int NT>
 __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __restrict__ E,
                                             const float* __restrict__ tab, const int (&xb)[R], const int (&ab)[R]) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q, QH = (Q + 1) / 2;
   float* const sT = reinterpret_cast<float*>(g_smem);
-  const int words = nodal_path_words(k, Q);
+  const int words = nodal_path_words(k, Q, NT);
   int slot[KM];
   float xv[R][KM];
   float2 acc[R][KM], ph0[R];
@@ -217,7 +220,7 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
         const int4 rec = Ep[s];
-        const float2* rho = tp + (3 * QP + s * 3 * QP) / 2;
+        const float2* rho = tp + (NT * QP + s * NT * QP) / 2;
         float2 rh[QH];
 #pragma unroll
         for (int h = 0; h < QH; ++h) rh[h] = rho[h];
@@ -244,7 +247,7 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        const float2* C = tp + (3 * QP + s * 3 * QP + QP) / 2;
+        const float2* C = tp + (NT * QP + s * NT * QP + QP) / 2;
         float2 Ch[QH];
 #pragma unroll
         for (int h = 0; h < QH; ++h) Ch[h] = C[h];
@@ -266,7 +269,7 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 }
 
 // One path, element loop not unrolled (large Q); accumulates per element.
-template <typename T, int Q, int R>
+template <typename T, int Q, int R, int NT>
 __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E, const T* __restrict__ tab,
                                               const int (&xb)[R], const int (&ab)[R]) {
   constexpr int QP = QP_<Q>::v;
@@ -287,7 +290,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
   for (int s = 0; s < k; ++s) {
     const int4 rec = E[s];
     T rho[Q];
-    lds_vec(rho, tab + 3 * QP + s * 3 * QP);
+    lds_vec(rho, tab + NT * QP + s * NT * QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool o = one_fraction(sT[xb[r] + rec.z], rec);
@@ -314,7 +317,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
   for (int s = 0; s < k; ++s) {
     const int sl = E[s].z;
     T C[Q];
-    lds_vec(C, tab + 3 * QP + s * 3 * QP + QP);
+    lds_vec(C, tab + NT * QP + s * NT * QP + QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       T a = ph0[r];
@@ -383,16 +386,22 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
   const int words = nodal_path_words(k, Q);
   T G[Q];
   lds_vec(G, gam);
-  int slot[KM], rb[KM];
-  T xv[R][KM];
+  // kLean: x, slot and row base are re-read from shared memory where used
+  // instead of living in registers for the whole run (register budget)
+  constexpr bool kLean = GTS_INTER_LEAN && kRegAcc;
+  constexpr int KS = kLean ? 1 : KM;
+  int slot[KS], rb[KS];
+  T xv[R][KS];
+  if constexpr (!kLean) {
 #pragma unroll
-  for (int s = 0; s < KM; ++s) {
-    const bool valid = (s < KM - 1 || s < k);
-    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
-    slot[s] = e.z;
-    rb[s] = e.w;
+    for (int s = 0; s < KM; ++s) {
+      const bool valid = (s < KM - 1 || s < k);
+      const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
+      slot[s] = e.z;
+      rb[s] = e.w;
 #pragma unroll
-    for (int r = 0; r < R; ++r) xv[r][s] = sT[xb[r] + e.z];
+      for (int r = 0; r < R; ++r) xv[r][s] = sT[xb[r] + e.z];
+    }
   }
   T acc[R][kRegAcc ? NC : 1];
 #pragma unroll
@@ -426,7 +435,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
         lds_vec(rho, tp + 3 * QP + s * 3 * QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const bool o = one_fraction(xv[r][s], rec);
+          const bool o = one_fraction(kLean ? sT[xb[r] + rec.z] : xv[r][KS == 1 ? 0 : s], rec);
           if (o) om[r] |= 1u << s;
           if (!o) {
 #pragma unroll
@@ -539,9 +548,11 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
     for (int i = 0; i < KM; ++i) {
 #pragma unroll
       for (int j = i; j < KM; ++j) {
-        if ((i < KM - 1 || i < k) && (j < KM - 1 || j < k))
+        if ((i < KM - 1 || i < k) && (j < KM - 1 || j < k)) {
+          const int cell = kLean ? E[i].w + E[j].z : rb[KS == 1 ? 0 : i] + slot[KS == 1 ? 0 : j];
 #pragma unroll
-          for (int r = 0; r < R; ++r) sT[ab[r] + rb[i] + slot[j]] += acc[r][c];
+          for (int r = 0; r < R; ++r) sT[ab[r] + cell] += acc[r][c];
+        }
         ++c;
       }
     }
@@ -563,15 +574,19 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
   float2 G[QH];
 #pragma unroll
   for (int h = 0; h < QH; ++h) G[h] = make_float2(gam[2 * h], 2 * h + 1 < Q ? gam[2 * h + 1] : 0.f);
-  int slot[KM], rb[KM];
-  float xv[KM];
+  constexpr bool kLean = GTS_INTER_LEAN;
+  constexpr int KS = kLean ? 1 : KM;
+  int slot[KS], rb[KS];
+  float xv[KS];
+  if constexpr (!kLean) {
 #pragma unroll
-  for (int s = 0; s < KM; ++s) {
-    const bool valid = (s < KM - 1 || s < k);
-    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
-    slot[s] = e.z;
-    rb[s] = e.w;
-    xv[s] = sT[xb[0] + e.z];
+    for (int s = 0; s < KM; ++s) {
+      const bool valid = (s < KM - 1 || s < k);
+      const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
+      slot[s] = e.z;
+      rb[s] = e.w;
+      xv[s] = sT[xb[0] + e.z];
+    }
   }
   float2 acc[NC];
 #pragma unroll
@@ -586,7 +601,8 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        const bool o = one_fraction(xv[s], Ep[s]);
+        const int4 rec = Ep[s];
+        const bool o = one_fraction(kLean ? sT[xb[0] + rec.z] : xv[KS == 1 ? 0 : s], rec);
         om |= (uint32_t)o << s;
         if (!o) {
           const float2* rho = tp + (3 * QP + s * 3 * QP) / 2;
@@ -642,7 +658,10 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
   for (int i = 0; i < KM; ++i) {
 #pragma unroll
     for (int j = i; j < KM; ++j) {
-      if ((i < KM - 1 || i < k) && (j < KM - 1 || j < k)) sT[ab[0] + rb[i] + slot[j]] += acc[c].x + acc[c].y;
+      if ((i < KM - 1 || i < k) && (j < KM - 1 || j < k)) {
+        const int cell = kLean ? E[i].w + E[j].z : rb[KS == 1 ? 0 : i] + slot[KS == 1 ? 0 : j];
+        sT[ab[0] + cell] += acc[c].x + acc[c].y;
+      }
       ++c;
     }
   }
@@ -709,18 +728,18 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
 // Small Q: all R rows of the lane at once (shared table loads, R-way ILP).
 // Larger Q: the lane's rows one after the other, which bounds the register
 // footprint of the whole kernel by the small-Q instantiations.
-template <typename T, int R, bool kInter>
+template <typename T, int R, bool kInter, int NT>
 __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E0, const T* __restrict__ table,
                                              const T* __restrict__ gauss, const int (&xb)[R], const int (&ab)[R]) {
   const int k = ph.x & 0xff, n_run = ph.x >> 16, q = ph.y;
   const int4* E = E0 + ph.z;
   const T* tab = table + ph.w;
-  const int words = nodal_path_words(k, q);
+  const int words = nodal_path_words(k, q, NT);
   if constexpr (!kInter && GTS_X2 && sizeof(T) == 4 && R <= 2) {
     // fp32: paired-node FFMA2 runs (Q >= 2); Q = 1 has nothing to pair
     switch (q) {
-      case 1: shap_run<T, 1, R>(k, n_run, E, tab, xb, ab); break;
-#define GTS_RUN(QQ) case QQ: shap_run_x2<QQ, R>(k, n_run, E, reinterpret_cast<const float*>(tab), xb, ab); break;
+      case 1: shap_run<T, 1, R, NT>(k, n_run, E, tab, xb, ab); break;
+#define GTS_RUN(QQ) case QQ: shap_run_x2<QQ, R, NT>(k, n_run, E, reinterpret_cast<const float*>(tab), xb, ab); break;
       GTS_RUN(2) GTS_RUN(3) GTS_RUN(4)
 #if GTS_X2_R2_QMAX >= 5
       GTS_RUN(5)
@@ -734,13 +753,13 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
         for (int r = 0; r < R; ++r) {
           const int xb1[1] = {xb[r]}, ab1[1] = {ab[r]};
           switch (q) {
-#define GTS_RUN1(QQ) case QQ: shap_run_x2<QQ, 1>(k, n_run, E, reinterpret_cast<const float*>(tab), xb1, ab1); break;
+#define GTS_RUN1(QQ) case QQ: shap_run_x2<QQ, 1, NT>(k, n_run, E, reinterpret_cast<const float*>(tab), xb1, ab1); break;
             GTS_RUN1(5) GTS_RUN1(6) GTS_RUN1(7) GTS_RUN1(8)
 #undef GTS_RUN1
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
-#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1>(k, E + p * k, tab + p * words, xb1, ab1); break;
+#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1, NT>(k, E + p * k, tab + p * words, xb1, ab1); break;
                   GTS_DYN(9) GTS_DYN(10) GTS_DYN(11) GTS_DYN(12) GTS_DYN(13) GTS_DYN(14) GTS_DYN(15) GTS_DYN(16)
 #undef GTS_DYN
                   default: break;
@@ -751,7 +770,7 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
     }
   } else if constexpr (!kInter) {
     switch (q) {
-#define GTS_RUN(QQ) case QQ: shap_run<T, QQ, R>(k, n_run, E, tab, xb, ab); break;
+#define GTS_RUN(QQ) case QQ: shap_run<T, QQ, R, NT>(k, n_run, E, tab, xb, ab); break;
       GTS_RUN(1) GTS_RUN(2) GTS_RUN(3) GTS_RUN(4)
 #undef GTS_RUN
       default:
@@ -759,13 +778,13 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
         for (int r = 0; r < R; ++r) {
           const int xb1[1] = {xb[r]}, ab1[1] = {ab[r]};
           switch (q) {
-#define GTS_RUN1(QQ) case QQ: shap_run<T, QQ, 1>(k, n_run, E, tab, xb1, ab1); break;
+#define GTS_RUN1(QQ) case QQ: shap_run<T, QQ, 1, NT>(k, n_run, E, tab, xb1, ab1); break;
             GTS_RUN1(5) GTS_RUN1(6) GTS_RUN1(7) GTS_RUN1(8)
 #undef GTS_RUN1
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
-#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1>(k, E + p * k, tab + p * words, xb1, ab1); break;
+#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1, NT>(k, E + p * k, tab + p * words, xb1, ab1); break;
                   GTS_DYN(9) GTS_DYN(10) GTS_DYN(11) GTS_DYN(12) GTS_DYN(13) GTS_DYN(14) GTS_DYN(15) GTS_DYN(16)
 #undef GTS_DYN
                   default: break;
@@ -793,7 +812,9 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
               }
               break;
             case 4:
-              if constexpr (GTS_INTER_Q2 && sizeof(T) == 4) {
+              if constexpr (GTS_INTER_Q2 == 3) {
+                inter_run<T, 4, 1, true>(k, n_run, E, tab, gam, xb1, ab1);
+              } else if constexpr (GTS_INTER_Q2 && sizeof(T) == 4) {
                 inter_run_q2<4>(k, n_run, E, reinterpret_cast<const float*>(tab),
                                 reinterpret_cast<const float*>(gam), xb1, ab1);
               } else {
@@ -1079,7 +1100,7 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
       const T* tab = reinterpret_cast<const T*>(sP + c.n_paths);
       for (int p = 0; p < c.n_paths;) {
         const int4 ph = sP[p];
-        run_dispatch<T, R, kInter>(ph, sE, tab, sT, xb, ab);
+        run_dispatch<T, R, kInter, nodal_tables(S)>(ph, sE, tab, sT, xb, ab);
         p += ph.x >> 16;
       }
       dirty = true;

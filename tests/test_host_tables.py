@@ -173,8 +173,9 @@ def test_nodal_blob_invariants(name, slots):
                 assert feats == feats0
                 np.testing.assert_array_equal(el[:, 3], el[:, 2] * (2 * hd["S"] - el[:, 2] - 1) // 2)
                 t, wq = g[Q - 1, 0, :Q], g[Q - 1, 1, :Q]
-                h = tab[t0 + 2 * QP:t0 + 2 * QP + Q]
-                v = float(2 * h[0] / wq[0])
+                nt = 2 if hd["S"] > 16 else 3  # SHAP-only blobs drop h and alpha (blob_format.h)
+                d = tab[t0 + QP:t0 + QP + Q]
+                v = float(-d[0] * (1 - t[0]) / wq[0])
                 cands = ref[feats]
                 best = min(range(len(cands)), key=lambda ii: abs(cands[ii][0] - v))
                 v, z = cands.pop(best)
@@ -182,13 +183,15 @@ def test_nodal_blob_invariants(name, slots):
                 B = z[:, None] * (1 - t[None])
                 np.testing.assert_allclose(tab[t0:t0 + Q], A.prod(axis=0), rtol=1e-12)
                 np.testing.assert_allclose(tab[t0 + QP:t0 + QP + Q], -v * wq / (1 - t), rtol=1e-12, atol=1e-300)
-                np.testing.assert_allclose(h, 0.5 * v * wq, rtol=1e-12, atol=1e-300)
-                rows = tab[t0 + 3 * QP:t0 + 3 * QP * (k + 1)].reshape(k, 3, QP)[:, :, :Q]
+                if nt == 3:
+                    np.testing.assert_allclose(tab[t0 + 2 * QP:t0 + 2 * QP + Q], 0.5 * v * wq, rtol=1e-12, atol=1e-300)
+                rows = tab[t0 + nt * QP:t0 + nt * QP * (k + 1)].reshape(k, nt, QP)[:, :, :Q]
                 np.testing.assert_allclose(rows[:, 0], B / A, rtol=1e-12)
                 # C' = C - d: the SHAP constant with the o = 0 share folded out (nodal.cuh shap_run)
                 np.testing.assert_allclose(rows[:, 1], v * wq[None] * ((1 - z[:, None]) / A + 1 / (1 - t[None])),
                                            rtol=1e-12, atol=1e-300)
-                np.testing.assert_allclose(rows[:, 2], (1 - z[:, None]) / A, rtol=1e-12, atol=1e-300)
+                if nt == 3:
+                    np.testing.assert_allclose(rows[:, 2], (1 - z[:, None]) / A, rtol=1e-12, atol=1e-300)
                 lo = E[e0:e0 + k, 0].view(np.float32)
                 assert np.all(lo == lo)  # bounds stored as fp32 bit patterns
                 seen += 1
