@@ -37,9 +37,6 @@
 #define GTS_INTER_Q2 2  // fp32 interaction runs on paired Gauss nodes: 1 = Q 3 and 4, 2 = Q 4 only
                         // (measured: 2 is best, +3 % cal_housing, +10 % adult; profiles/r01i)
 #endif
-#ifndef GTS_INTER_LEAN
-#define GTS_INTER_LEAN 0  // register-resident interaction runs re-read x / slots from shared (A/B knob)
-#endif
 #ifndef GTS_X2_R2_QMAX
 #define GTS_X2_R2_QMAX 6  // largest Q whose paired-node SHAP run keeps both rows of a lane in flight
                           // (measured: adult SHAP +19 % for 6 over 4; profiles/r01h)
@@ -386,22 +383,16 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
   const int words = nodal_path_words(k, Q);
   T G[Q];
   lds_vec(G, gam);
-  // kLean: x, slot and row base are re-read from shared memory where used
-  // instead of living in registers for the whole run (register budget)
-  constexpr bool kLean = GTS_INTER_LEAN && kRegAcc;
-  constexpr int KS = kLean ? 1 : KM;
-  int slot[KS], rb[KS];
-  T xv[R][KS];
-  if constexpr (!kLean) {
+  int slot[KM], rb[KM];
+  T xv[R][KM];
 #pragma unroll
-    for (int s = 0; s < KM; ++s) {
-      const bool valid = (s < KM - 1 || s < k);
-      const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
-      slot[s] = e.z;
-      rb[s] = e.w;
+  for (int s = 0; s < KM; ++s) {
+    const bool valid = (s < KM - 1 || s < k);
+    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
+    slot[s] = e.z;
+    rb[s] = e.w;
 #pragma unroll
-      for (int r = 0; r < R; ++r) xv[r][s] = sT[xb[r] + e.z];
-    }
+    for (int r = 0; r < R; ++r) xv[r][s] = sT[xb[r] + e.z];
   }
   T acc[R][kRegAcc ? NC : 1];
 #pragma unroll
@@ -435,7 +426,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
         lds_vec(rho, tp + 3 * QP + s * 3 * QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const bool o = one_fraction(kLean ? sT[xb[r] + rec.z] : xv[r][KS == 1 ? 0 : s], rec);
+          const bool o = one_fraction(xv[r][s], rec);
           if (o) om[r] |= 1u << s;
           if (!o) {
 #pragma unroll
@@ -548,11 +539,9 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
     for (int i = 0; i < KM; ++i) {
 #pragma unroll
       for (int j = i; j < KM; ++j) {
-        if ((i < KM - 1 || i < k) && (j < KM - 1 || j < k)) {
-          const int cell = kLean ? E[i].w + E[j].z : rb[KS == 1 ? 0 : i] + slot[KS == 1 ? 0 : j];
+        if ((i < KM - 1 || i < k) && (j < KM - 1 || j < k))
 #pragma unroll
-          for (int r = 0; r < R; ++r) sT[ab[r] + cell] += acc[r][c];
-        }
+          for (int r = 0; r < R; ++r) sT[ab[r] + rb[i] + slot[j]] += acc[r][c];
         ++c;
       }
     }
@@ -574,19 +563,15 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
   float2 G[QH];
 #pragma unroll
   for (int h = 0; h < QH; ++h) G[h] = make_float2(gam[2 * h], 2 * h + 1 < Q ? gam[2 * h + 1] : 0.f);
-  constexpr bool kLean = GTS_INTER_LEAN;
-  constexpr int KS = kLean ? 1 : KM;
-  int slot[KS], rb[KS];
-  float xv[KS];
-  if constexpr (!kLean) {
+  int slot[KM], rb[KM];
+  float xv[KM];
 #pragma unroll
-    for (int s = 0; s < KM; ++s) {
-      const bool valid = (s < KM - 1 || s < k);
-      const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
-      slot[s] = e.z;
-      rb[s] = e.w;
-      xv[s] = sT[xb[0] + e.z];
-    }
+  for (int s = 0; s < KM; ++s) {
+    const bool valid = (s < KM - 1 || s < k);
+    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
+    slot[s] = e.z;
+    rb[s] = e.w;
+    xv[s] = sT[xb[0] + e.z];
   }
   float2 acc[NC];
 #pragma unroll
@@ -601,8 +586,7 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        const int4 rec = Ep[s];
-        const bool o = one_fraction(kLean ? sT[xb[0] + rec.z] : xv[KS == 1 ? 0 : s], rec);
+        const bool o = one_fraction(xv[s], Ep[s]);
         om |= (uint32_t)o << s;
         if (!o) {
           const float2* rho = tp + (3 * QP + s * 3 * QP) / 2;
@@ -658,10 +642,7 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
   for (int i = 0; i < KM; ++i) {
 #pragma unroll
     for (int j = i; j < KM; ++j) {
-      if ((i < KM - 1 || i < k) && (j < KM - 1 || j < k)) {
-        const int cell = kLean ? E[i].w + E[j].z : rb[KS == 1 ? 0 : i] + slot[KS == 1 ? 0 : j];
-        sT[ab[0] + cell] += acc[c].x + acc[c].y;
-      }
+      if ((i < KM - 1 || i < k) && (j < KM - 1 || j < k)) sT[ab[0] + rb[i] + slot[j]] += acc[c].x + acc[c].y;
       ++c;
     }
   }
@@ -812,9 +793,7 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
               }
               break;
             case 4:
-              if constexpr (GTS_INTER_Q2 == 3) {
-                inter_run<T, 4, 1, true>(k, n_run, E, tab, gam, xb1, ab1);
-              } else if constexpr (GTS_INTER_Q2 && sizeof(T) == 4) {
+              if constexpr (GTS_INTER_Q2 && sizeof(T) == 4) {
                 inter_run_q2<4>(k, n_run, E, reinterpret_cast<const float*>(tab),
                                 reinterpret_cast<const float*>(gam), xb1, ab1);
               } else {
