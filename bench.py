@@ -5,9 +5,12 @@ number through the public API.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload cal_housing-med] [--rows-per-gpu 1048576] [--mode both|shap|interactions]
 
-One "step" = one pass of the per-row hot path over this rank's batch of rows:
-gts_shap (SHAP values + bias) and gts_shap_interactions (interaction values),
-with the packed path table resident (extract -> pack -> blob runs once per model,
+One "step" = one pass of the per-row hot path over this rank's batch of rows
+producing the SHAP values + bias and the interaction values: in mode "both"
+one gts_shap_and_interactions call (the interaction kernel also writes phi;
+`--separate` times gts_shap + gts_shap_interactions instead, which the line
+reports beside it as "both.separate_*", and "shap" / "interactions" time each
+kernel alone), with the packed path table resident (extract -> pack -> blob runs once per model,
 PAPER.md:528, and is reported as `preprocess_ms`).  Rows are sharded across
 ranks (weak scaling); the blob is replicated by ONE NCCL broadcast.  Rank 0
 prints one JSON line.
@@ -63,6 +66,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ablation", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--separate", action="store_true",
+                    help="mode both: time the step as gts_shap + gts_shap_interactions instead of the fused "
+                         "gts_shap_and_interactions call")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     return ap.parse_args()
 
@@ -301,6 +307,16 @@ def run_ours(args):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    fused = args.mode == "both" and not args.separate
+
+    def fused_step(evs=None):
+        if evs: evs[4].record(stream)
+        for r0 in range(0, n, ij_chunk):
+            xr = xd[r0:r0 + ij_chunk]
+            gts.gts_shap_and_interactions(info_i, ex.blob_int.ptr, xr.data_ptr(), xr.shape[0], x_rs, x_cs,
+                                          phi[r0:r0 + ij_chunk].data_ptr(), phi_ij.data_ptr(), stream.cuda_stream)
+        if evs: evs[5].record(stream)
+
     def step(evs=None):
         if do_shap:
             if evs: evs[0].record(stream)
@@ -317,26 +333,33 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         step()
+        if fused:
+            fused_step()
     torch.cuda.synchronize()
     gpu_uuid = str(torch.cuda.get_device_properties(dev).uuid)
     gpu_id = gpu_uuid if gpu_uuid.startswith("GPU-") else "GPU-" + gpu_uuid
-    t_step, t_shap, t_int = [], [], []
+    t_step, t_shap, t_int, t_sep = [], [], [], []
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(gpu_id) as clk:
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the events)
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
             step(evs)
+            if fused:
+                flush.zero_()
+                fused_step(evs)
             torch.cuda.synchronize()
             ts = evs[0].elapsed_time(evs[1]) if do_shap else 0.0
             ti = evs[2].elapsed_time(evs[3]) if do_int else 0.0
             t_shap.append(ts)
             t_int.append(ti)
-            t_step.append(ts + ti)
+            t_sep.append(ts + ti)
+            t_step.append(evs[4].elapsed_time(evs[5]) if fused else ts + ti)
     torch.cuda.synchronize()
     barrier(world)
     ms_step = max_over_ranks(float(np.mean(t_step)), world)
+    ms_sep = max_over_ranks(float(np.mean(t_sep)), world)
     ms_shap = max_over_ranks(float(np.mean(t_shap)), world)
     ms_int = max_over_ranks(float(np.mean(t_int)), world)
     clocks = clk.summary()
@@ -352,6 +375,14 @@ def run_ours(args):
 
         def e2e_step():
             xe.copy_(x_pin, non_blocking=True)
+            if fused:
+                for r0 in range(0, n, e2e_chunk):
+                    r1 = min(n, r0 + e2e_chunk)
+                    ex.shap_and_interactions_device(xe[r0:r1], out_phi=phi[r0:r1], out_phi_ij=phi_ij[: r1 - r0],
+                                                    stream=stream)
+                    phi_ij_h[: r1 - r0].copy_(phi_ij[: r1 - r0], non_blocking=True)
+                phi_h.copy_(phi, non_blocking=True)
+                return
             if do_shap:
                 ex.shap_device(xe, out=phi, stream=stream)
                 phi_h.copy_(phi, non_blocking=True)
@@ -377,7 +408,9 @@ def run_ours(args):
         d2h = (phi.numel() * phi.element_size() if do_shap else 0) + (n * ij_row_bytes if do_int else 0)
         e2e = {"value": world * n / (ms_e2e / 1000.0), "unit": "rows/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e,
-               "api": "TreeShapExplainer.shap_device/interactions_device with pinned host X and phi (H2D + D2H)"}
+               "api": ("TreeShapExplainer.shap_and_interactions_device" if fused else
+                       "TreeShapExplainer.shap_device/interactions_device") +
+                      " with pinned host X and phi (H2D + D2H)"}
 
     # --- ablation: the paper-lineage warp-bin kernels on a slice of the rows
     ablation = None
@@ -449,9 +482,16 @@ def run_ours(args):
     r_shap = roof(info_s.shap_flops_per_row, info_s.paper_shap_flops_per_row, ms_shap) if do_shap else None
     r_int = roof(info_i.inter_flops_per_row, info_i.paper_inter_flops_per_row, ms_int) if do_int else None
     dominant = "interactions" if (do_int and ms_int >= ms_shap) else "shap"
-    roofline = dict((r_int if dominant == "interactions" else r_shap) or {})
-    roofline["kernel"] = ("gts_shap_interactions" if dominant == "interactions" else "gts_shap") + \
-        f" ({args.layout} kernel + init fill, CUDA events on the launch stream)"
+    if fused:
+        # the step is the fused call: the interaction kernel's work, phi read off its diagonal
+        r_both = roof(info_i.inter_flops_per_row, info_i.paper_inter_flops_per_row, ms_step)
+        roofline = dict(r_both)
+        roofline["kernel"] = (f"gts_shap_and_interactions ({args.layout} interaction kernel writing phi and phi_ij "
+                              "+ init fills, CUDA events on the launch stream)")
+    else:
+        roofline = dict((r_int if dominant == "interactions" else r_shap) or {})
+        roofline["kernel"] = ("gts_shap_interactions" if dominant == "interactions" else "gts_shap") + \
+            f" ({args.layout} kernel + init fill, CUDA events on the launch stream)"
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         try:
@@ -461,8 +501,9 @@ def run_ours(args):
                 roofline["traffic_source"] = tr.get("source")
         except Exception:
             pass
-    launches = (gts.gts_launches_per_call(info_s, False) if do_shap else 0) + (
+    launches_sep = (gts.gts_launches_per_call(info_s, False) if do_shap else 0) + (
         gts.gts_launches_per_call(info_i, True) * -(-n // ij_chunk) if do_int else 0)
+    launches = gts.gts_launches_per_call(info_i, 2) * -(-n // ij_chunk) if fused else launches_sep
     line = {
         "metric": METRIC,
         "value": total_rows / (ms_step / 1000.0),
@@ -487,6 +528,10 @@ def run_ours(args):
         "shap": {"rows_per_s": total_rows / (ms_shap / 1000.0), "ms": ms_shap, "roofline": r_shap} if do_shap else None,
         "interactions": {"rows_per_s": total_rows / (ms_int / 1000.0), "ms": ms_int, "roofline": r_int}
         if do_int else None,
+        "both": ({"rows_per_s": total_rows / (ms_step / 1000.0), "ms": ms_step,
+                  "call": "gts_shap_and_interactions (one pass: phi and phi_ij)",
+                  "separate_rows_per_s": total_rows / (ms_sep / 1000.0), "separate_ms": ms_sep,
+                  "separate_launches_per_step": launches_sep} if fused else None),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,

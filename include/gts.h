@@ -222,7 +222,23 @@ gts_status gts_shap_interactions_strided(const gts_blob_info* info, const void* 
                                          int64_t n_rows, int64_t row_stride, int64_t col_stride, void* d_phi_ij,
                                          void* stream);
 
-/* Number of kernel launches one gts_shap / gts_shap_interactions call issues. */
+/* SHAP values and SHAP interaction values of the same rows in one pass.
+   Outputs are those of gts_shap_strided (d_phi) and
+   gts_shap_interactions_strided (d_phi_ij), both fully overwritten; strides as
+   above.  info must describe an interaction-capable blob (NODAL with
+   max_slots <= 16, or WARP_BINS).  NODAL: phi is not computed by the SHAP
+   kernel but read off the interaction pass: per path, the diagonal
+   accumulator of the interaction kernel holds phi_i = v (o_i - z_i) U_i
+   (Algorithm 1) before Eq. 6 turns it into
+   phi_ii, so the tile flush adds it to phi too (one extra atomic per non-zero
+   (row, group, feature) per flush).  WARP_BINS: the two kernels back to back.
+   Errors as gts_shap_interactions; d_phi and d_phi_ij must not overlap. */
+gts_status gts_shap_and_interactions(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
+                                     int64_t row_stride, int64_t col_stride, void* d_phi, void* d_phi_ij,
+                                     void* stream);
+
+/* Number of kernel launches one call issues: interactions = 0 for gts_shap,
+   1 for gts_shap_interactions, 2 for gts_shap_and_interactions. */
 int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions);
 
 const char* gts_last_error(void);

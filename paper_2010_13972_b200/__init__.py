@@ -6,10 +6,10 @@ by ``_build.build()``); ``gts`` is its thin ctypes binding with the same names,
 """
 from . import gts  # noqa: F401
 from .gts import (gts_binpack, gts_blob_plan, gts_blob_write, gts_extract_paths,  # noqa: F401
-                  gts_shap, gts_shap_interactions)
+                  gts_shap, gts_shap_and_interactions, gts_shap_interactions)
 
 __all__ = ["gts", "gts_extract_paths", "gts_binpack", "gts_blob_plan", "gts_blob_write", "gts_shap",
-           "gts_shap_interactions", "TreeShapExplainer"]
+           "gts_shap_interactions", "gts_shap_and_interactions", "TreeShapExplainer"]
 
 
 def __getattr__(name):

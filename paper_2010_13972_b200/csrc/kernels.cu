@@ -119,7 +119,7 @@ size_t nodal_smem_bytes(const gts_blob_info* info) {
 
 template <typename T, bool kInter, int S>
 gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const void* d_X, int64_t n_rows, int64_t rs,
-                        int64_t cs, void* out, cudaStream_t st) {
+                        int64_t cs, void* out, cudaStream_t st, void* out_phi = nullptr) {
   constexpr int W = nodal::Cfg<T, kInter, S>::W;
   constexpr int R = nodal::Cfg<T, kInter, S>::R;
   auto kern = nodal::nodal_kernel<T, S, W, R, kInter>;
@@ -154,6 +154,7 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   a.row_stride = rs;
   a.col_stride = cs;
   a.out = out;
+  a.out_phi = out_phi;
   a.n_splits = (int)splits;
   a.M = info->n_features;
   a.G = info->n_groups;
@@ -168,10 +169,10 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
 
 template <typename T, bool kInter>
 gts_status launch_nodal_s(const gts_blob_info* info, const char* d_blob, const void* d_X, int64_t n_rows,
-                          int64_t rs, int64_t cs, void* out, cudaStream_t st) {
+                          int64_t rs, int64_t cs, void* out, cudaStream_t st, void* out_phi = nullptr) {
   switch (info->max_slots) {
-    case 8: return launch_nodal<T, kInter, 8>(info, d_blob, d_X, n_rows, rs, cs, out, st);
-    case 16: return launch_nodal<T, kInter, 16>(info, d_blob, d_X, n_rows, rs, cs, out, st);
+    case 8: return launch_nodal<T, kInter, 8>(info, d_blob, d_X, n_rows, rs, cs, out, st, out_phi);
+    case 16: return launch_nodal<T, kInter, 16>(info, d_blob, d_X, n_rows, rs, cs, out, st, out_phi);
     case 32:
       if constexpr (kInter) break;
       else return launch_nodal<T, kInter, 32>(info, d_blob, d_X, n_rows, rs, cs, out, st);
@@ -250,6 +251,33 @@ gts_status run(const gts_blob_info* info, const void* d_blob, const void* d_X, i
              : launch_bins<double, kInter>(info, blob, d_X, n_rows, rs, cs, d_out, st);
 }
 
+// SHAP and interaction values in one pass (NODAL): the interaction kernel's
+// diagonal cells hold each tile's sum of phi_i before Eq. 6 is applied, so the
+// flush adds them to phi as well; no SHAP kernel runs.  WARP_BINS blobs run
+// their two kernels back to back.
+gts_status run_fused(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows, int64_t rs,
+                     int64_t cs, void* d_phi, void* d_phi_ij, void* stream) {
+  gts_status s = check_call(info, d_blob, d_X, n_rows, rs, cs, d_phi_ij);
+  if (s != GTS_OK || n_rows == 0) return s;
+  s = check_call(info, d_blob, d_X, n_rows, rs, cs, d_phi);
+  if (s != GTS_OK) return s;
+  if (info->layout != GTS_LAYOUT_NODAL) {
+    s = run<true>(info, d_blob, d_X, n_rows, rs, cs, d_phi_ij, stream);
+    return s != GTS_OK ? s : run<false>(info, d_blob, d_X, n_rows, rs, cs, d_phi, stream);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const char* blob = static_cast<const char*>(d_blob);
+  const bool f32 = info->dtype == GTS_F32;
+  s = f32 ? launch_init<float>(true, info, blob, n_rows, d_phi_ij, st)
+          : launch_init<double>(true, info, blob, n_rows, d_phi_ij, st);
+  if (s != GTS_OK) return s;
+  s = f32 ? launch_init<float>(false, info, blob, n_rows, d_phi, st)
+          : launch_init<double>(false, info, blob, n_rows, d_phi, st);
+  if (s != GTS_OK) return s;
+  return f32 ? launch_nodal_s<float, true>(info, blob, d_X, n_rows, rs, cs, d_phi_ij, st, d_phi)
+             : launch_nodal_s<double, true>(info, blob, d_X, n_rows, rs, cs, d_phi_ij, st, d_phi);
+}
+
 }  // namespace
 }  // namespace gts
 
@@ -276,10 +304,18 @@ gts_status gts_shap_interactions_strided(const gts_blob_info* info, const void* 
   return gts::run<true>(info, d_blob, d_X, n_rows, row_stride, col_stride, d_phi_ij, stream);
 }
 
+gts_status gts_shap_and_interactions(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
+                                     int64_t row_stride, int64_t col_stride, void* d_phi, void* d_phi_ij,
+                                     void* stream) {
+  return gts::run_fused(info, d_blob, d_X, n_rows, row_stride, col_stride, d_phi, d_phi_ij, stream);
+}
+
 int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions) {
-  (void)interactions;
   if (!info) return 0;
-  return info->n_units > 0 ? 2 : 1;  // init + main kernel
+  const int32_t main = info->n_units > 0 ? 1 : 0;
+  if (interactions == 2)  // gts_shap_and_interactions
+    return info->layout == GTS_LAYOUT_NODAL ? 2 + main : 2 + 2 * main;
+  return 1 + main;  // init + main kernel
 }
 
 }  // extern "C"

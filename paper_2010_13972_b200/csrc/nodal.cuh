@@ -833,6 +833,7 @@ struct Args {
   int64_t n_rows;
   int64_t row_stride, col_stride;  // X[r][f] at X[r * row_stride + f * col_stride]
   void* out;
+  void* out_phi;  // interaction kernel only: if set, the phi_i cells are also added to phi (fused call)
   int n_splits;
   int M, G;
   int64_t n_chunks;
@@ -988,6 +989,9 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
               if (j != i) rowsum += tile[j < i ? tri_row_base(j, S) + i : rbi + j];
             const T d = tile[rbi + i] - rowsum;
             if (d != (T)0) atomicAdd(base + (size_t)fi * M1 + fi, d);
+            // fused call: the diagonal cell before Eq. 6 is the tile's SHAP value phi_i
+            if (a.out_phi != nullptr && tile[rbi + i] != (T)0)
+              atomicAdd(static_cast<T*>(a.out_phi) + ((size_t)rg * a.G + cur_group) * M1 + fi, tile[rbi + i]);
             for (int j = i + 1; j < cur_slots; ++j) {
               const T v = tile[rbi + j];
               if (v != (T)0) {

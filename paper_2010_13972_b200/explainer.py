@@ -124,6 +124,22 @@ class TreeShapExplainer:
                                           out.data_ptr(), st.cuda_stream)
         return out
 
+    def shap_and_interactions_device(self, X: torch.Tensor, out_phi: torch.Tensor | None = None,
+                                     out_phi_ij: torch.Tensor | None = None, stream=None):
+        """(phi, phi_ij) of the same rows from one pass (gts_shap_and_interactions):
+        the interaction kernel also writes the SHAP values, no SHAP kernel runs."""
+        n = X.shape[0]
+        M1 = self.n_features + 1
+        if out_phi is None:
+            out_phi = torch.empty((n, self.n_groups, M1), dtype=self.torch_dtype, device=self.device)
+        if out_phi_ij is None:
+            out_phi_ij = torch.empty((n, self.n_groups, M1, M1), dtype=self.torch_dtype, device=self.device)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rs, cs = self._strides(X)
+        gts.gts_shap_and_interactions(self.blob_int.info, self.blob_int.ptr, X.data_ptr(), n, rs, cs,
+                                      out_phi.data_ptr(), out_phi_ij.data_ptr(), st.cuda_stream)
+        return out_phi, out_phi_ij
+
     def graphed(self, n_rows: int, interactions: bool = False) -> "GraphedCall":
         """Latency regime: capture one call for
         a fixed row count into a CUDA graph over static X / output buffers, so
@@ -163,6 +179,12 @@ class TreeShapExplainer:
     def shap_interactions(self, X) -> np.ndarray:
         Xd = self._device_x(X)
         return self.interactions_device(Xd).cpu().numpy()
+
+    def shap_and_interactions(self, X) -> tuple[np.ndarray, np.ndarray]:
+        """End to end from host X: (phi, phi_ij) from one device pass."""
+        Xd = self._device_x(X)
+        phi, phi_ij = self.shap_and_interactions_device(Xd)
+        return phi.cpu().numpy(), phi_ij.cpu().numpy()
 
 
 class GraphedCall:

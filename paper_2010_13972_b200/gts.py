@@ -77,7 +77,7 @@ class gts_blob_info(ctypes.Structure):
 # The symbols the header declares (checked by tests/test_abi.py).
 EXPORTS = ["gts_extract_paths", "gts_paths_view_get", "gts_paths_free", "gts_binpack", "gts_bins_view_get",
            "gts_bins_free", "gts_blob_plan", "gts_blob_write", "gts_shap", "gts_shap_interactions",
-           "gts_shap_strided", "gts_shap_interactions_strided",
+           "gts_shap_strided", "gts_shap_interactions_strided", "gts_shap_and_interactions",
            "gts_launches_per_call", "gts_last_error", "gts_status_string", "gts_abi_version"]
 
 _lib = None
@@ -110,6 +110,8 @@ def load(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = [P(gts_blob_info), _vp, _vp, _i64, _i64, _i64, _vp, _vp]
         fn.restype = ctypes.c_int
+    lib.gts_shap_and_interactions.argtypes = [P(gts_blob_info), _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]
+    lib.gts_shap_and_interactions.restype = ctypes.c_int
     lib.gts_launches_per_call.argtypes = [P(gts_blob_info), _i32]
     lib.gts_launches_per_call.restype = _i32
     lib.gts_last_error.argtypes = []
@@ -256,5 +258,14 @@ def gts_shap_interactions_strided(info: gts_blob_info, d_blob: int, d_x: int, n_
                                                 int(col_stride), d_phi_ij, stream or None))
 
 
-def gts_launches_per_call(info: gts_blob_info, interactions: bool) -> int:
-    return int(load().gts_launches_per_call(ctypes.byref(info), int(bool(interactions))))
+def gts_shap_and_interactions(info: gts_blob_info, d_blob: int, d_x: int, n_rows: int, row_stride: int,
+                              col_stride: int, d_phi: int, d_phi_ij: int, stream: int = 0):
+    """(3)+(4) in one pass: SHAP values and interaction values of the same rows."""
+    _check(load().gts_shap_and_interactions(ctypes.byref(info), d_blob, d_x, int(n_rows), int(row_stride),
+                                            int(col_stride), d_phi, d_phi_ij, stream or None))
+
+
+def gts_launches_per_call(info: gts_blob_info, interactions) -> int:
+    """Kernel launches per call: interactions False/0 = gts_shap, True/1 = gts_shap_interactions,
+    2 = gts_shap_and_interactions."""
+    return int(load().gts_launches_per_call(ctypes.byref(info), int(interactions)))

@@ -119,12 +119,22 @@ def test_blob_plan_and_call_argument_errors():
     bad = gts.gts_blob_info.from_bytes(info.to_bytes())
     bad.magic = 0
     assert _status(gts.gts_shap_interactions, bad, 16, 16, 4, 2, 16) == 1
+    # fused call: both outputs are checked (row-major strides (2, 1))
+    gts.gts_shap_and_interactions(info, 0, 0, 0, 2, 1, 0, 0)
+    assert _status(gts.gts_shap_and_interactions, info, 16, 16, 4, 2, 1, 0, 16) == 1   # NULL phi
+    assert _status(gts.gts_shap_and_interactions, info, 16, 16, 4, 2, 1, 16, 0) == 1   # NULL phi_ij
+    assert _status(gts.gts_shap_and_interactions, info, 16, 16, 4, 2, 1, 18, 16) == 1  # misaligned phi
+    assert _status(gts.gts_shap_and_interactions, bad, 16, 16, 4, 2, 1, 16, 16) == 1
 
 
 def test_launch_count_and_info_roundtrip():
     b = gts.gts_binpack(gts.gts_extract_paths(synth.depth2()), 32, "bfd")
     info = gts.gts_blob_plan(b, gts.GTS_F64, "warp_bins")
     assert gts.gts_launches_per_call(info, False) == 2
+    assert gts.gts_launches_per_call(info, True) == 2
+    assert gts.gts_launches_per_call(info, 2) == 4  # WARP_BINS fused: both calls back to back
+    nodal = gts.gts_blob_plan(b, gts.GTS_F32, "nodal")
+    assert gts.gts_launches_per_call(nodal, 2) == 3  # two init fills + the interaction kernel
     again = gts.gts_blob_info.from_bytes(info.to_bytes())
     assert again.as_dict() == info.as_dict()
 

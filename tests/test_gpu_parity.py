@@ -109,6 +109,53 @@ def test_configs_interactions(gpu, case, dtype, layout):
     parity.check(got, ref, dtype, f"{name} interactions")
 
 
+# ------------------------------------------------- fused SHAP + interactions
+
+FUSED = [c[:1] + (c[3], c[2]) for c in CASES if c[3] > 0] + [("fashion_mnist-med", 4, 120)]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("case", FUSED, ids=[c[0] for c in FUSED])
+def test_fused_shap_and_interactions(gpu, case, dtype, layout):
+    """gts_shap_and_interactions: phi read off the interaction pass (NODAL) must
+    match O5 and phi_ij must match O6, like the two separate calls."""
+    import torch
+    name, n, trees = case
+    w = WORKLOADS[name]
+    ens = w.ensemble()
+    if trees is not None:
+        ens = ens.subset(range(trees))
+    x = w.x(n, ens=ens)
+    ex = _explainer(ens, dtype, layout)
+    xd = torch.from_numpy(np.ascontiguousarray(x, dtype=ex.np_dtype)).cuda()
+    phi, phi_ij = ex.shap_and_interactions_device(xd)
+    torch.cuda.synchronize()
+    x64 = x.astype(np.float64)
+    parity.check(phi.cpu().numpy(), oracle.treeshap(ens, x64), dtype, f"{name} fused shap")
+    parity.check(phi_ij.cpu().numpy(), oracle.interactions(ens, x64), dtype, f"{name} fused interactions")
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_fused_ragged_and_feature_major(gpu, layout):
+    import torch
+    from paper_2010_13972_b200 import gts
+    w = WORKLOADS["cal_housing-med"]
+    ens = w.ensemble().subset(range(25))
+    ex = _explainer(ens, "f32", layout)
+    assert gts.gts_launches_per_call(ex.blob_int.info, 2) == (3 if layout == "nodal" else 4)
+    for n in (0, 1, 33, 300):
+        x = w.x(n, ens=ens)
+        for fm in (False, True):
+            xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t() if fm else torch.from_numpy(x).cuda()
+            phi, phi_ij = ex.shap_and_interactions_device(xd)
+            torch.cuda.synchronize()
+            if n:
+                x64 = x.astype(np.float64)
+                parity.check(phi.cpu().numpy(), oracle.treeshap(ens, x64), "f32", f"n={n} fm={fm}")
+                parity.check(phi_ij.cpu().numpy(), oracle.interactions(ens, x64), "f32", f"n={n} fm={fm} ij")
+
+
 # ------------------------------------------------------------------ edges
 
 @pytest.mark.parametrize("layout", LAYOUTS)
