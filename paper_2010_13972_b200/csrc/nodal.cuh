@@ -33,9 +33,12 @@
 #define GTS_INTER_R8 1  // rows per lane of the fp32 interaction kernel with 8 slots
                         // (measured: 1 row, 8 warps per block beats 2 rows, 4 warps by 8 %; profiles/r01h)
 #endif
-#ifndef GTS_INTER_Q2
-#define GTS_INTER_Q2 2  // fp32 interaction runs on paired Gauss nodes: 1 = Q 3 and 4, 2 = Q 4 only
-                        // (measured: 2 is best, +3 % cal_housing, +10 % adult; profiles/r01i)
+#ifndef GTS_INTER_PAIRED
+#define GTS_INTER_PAIRED ((1 << 2) | (1 << 4))  // bit Q: fp32 interaction runs with Q nodes use paired
+                                                // Gauss nodes (inter_run_q2).  Measured: Q = 4 +3 % cal_housing,
+                                                // +10 % adult (profiles/r01i); Q = 2 another +3 % cal_housing;
+                                                // Q = 3 (pair + scalar tail) -4 %, padded to 4 nodes -14 %
+                                                // (profiles/r01n, r01i)
 #endif
 #ifndef GTS_X2_R2_QMAX
 #define GTS_X2_R2_QMAX 6  // largest Q whose paired-node SHAP run keeps both rows of a lane in flight
@@ -551,18 +554,21 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
 // fp32, one row: inter_run on packed pairs of Gauss nodes.  Every cell keeps
 // an {even node, odd node} partial sum, so the pair products, the diagonal
 // sums, W and y run on paired FP32 instructions (FFMA2 / FMUL2) and the run's
-// cells stay in registers even for Q = 4 (where the scalar version writes each
-// pair to the shared tile).  Pads q >= Q are zero in the table (P_pad = 0).
+// cells stay in registers.  Odd Q: the last node is a scalar "tail" whose
+// products accumulate into the .x half of the same cell (no padded node).
 template <int Q>
 __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __restrict__ E,
                                              const float* __restrict__ tab, const float* __restrict__ gam,
                                              const int (&xb)[1], const int (&ab)[1]) {
-  constexpr int QP = QP_<Q>::v, KM = 2 * Q, NC = KM * (KM + 1) / 2, QH = (Q + 1) / 2;
+  constexpr int QP = QP_<Q>::v, KM = 2 * Q, NC = KM * (KM + 1) / 2, NP = Q / 2;
+  constexpr bool kTail = (Q & 1) != 0;
+  constexpr int TQ = Q - 1;  // the tail node (odd Q)
   float* const sT = reinterpret_cast<float*>(g_smem);
   const int words = nodal_path_words(k, Q);
-  float2 G[QH];
+  float2 G[NP > 0 ? NP : 1];
 #pragma unroll
-  for (int h = 0; h < QH; ++h) G[h] = make_float2(gam[2 * h], 2 * h + 1 < Q ? gam[2 * h + 1] : 0.f);
+  for (int h = 0; h < NP; ++h) G[h] = make_float2(gam[2 * h], gam[2 * h + 1]);
+  const float Gt = kTail ? gam[TQ] : 0.f;
   int slot[KM], rb[KM];
   float xv[KM];
 #pragma unroll
@@ -578,10 +584,12 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
   for (int c = 0; c < NC; ++c) acc[c] = make_float2(0.f, 0.f);
   for (int p = 0; p < n_run; ++p) {
     const int4* Ep = E + p * k;
-    const float2* tp = reinterpret_cast<const float2*>(tab + p * words);
-    float2 P[QH];
+    const float* tf = tab + p * words;
+    const float2* tp = reinterpret_cast<const float2*>(tf);
+    float2 P[NP > 0 ? NP : 1];
 #pragma unroll
-    for (int h = 0; h < QH; ++h) P[h] = tp[h];
+    for (int h = 0; h < NP; ++h) P[h] = tp[h];
+    float Pt = kTail ? tf[TQ] : 0.f;
     uint32_t om = 0u;
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
@@ -589,45 +597,55 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
         const bool o = one_fraction(xv[s], Ep[s]);
         om |= (uint32_t)o << s;
         if (!o) {
-          const float2* rho = tp + (3 * QP + s * 3 * QP) / 2;
+          const float* rho = tf + 3 * QP + s * 3 * QP;
 #pragma unroll
-          for (int h = 0; h < QH; ++h) P[h] = __fmul2_rn(P[h], rho[h]);  // EXTEND at the nodes
+          for (int h = 0; h < NP; ++h) P[h] = __fmul2_rn(P[h], reinterpret_cast<const float2*>(rho)[h]);  // EXTEND
+          if constexpr (kTail) Pt *= rho[TQ];
         }
       }
     }
-    float2 W[QH];
+    float2 W[NP > 0 ? NP : 1];
 #pragma unroll
-    for (int h = 0; h < QH; ++h) W[h] = __fmul2_rn(P[h], tp[QP + h]);  // h_q = v w_q / 2
-    float2 u[KM][QH];
+    for (int h = 0; h < NP; ++h) W[h] = __fmul2_rn(P[h], tp[QP + h]);  // h_q = v w_q / 2
+    const float Wt = kTail ? Pt * tf[2 * QP + TQ] : 0.f;
+    float2 u[KM][NP > 0 ? NP : 1];
+    float ut[KM];
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        const float2* al = tp + (3 * QP + s * 3 * QP + 2 * QP) / 2;
+        const float* al = tf + 3 * QP + s * 3 * QP + 2 * QP;
         const bool o = (om >> s) & 1u;
 #pragma unroll
-        for (int h = 0; h < QH; ++h) {
-          const float2 a = al[h];
+        for (int h = 0; h < NP; ++h) {
+          const float2 a = reinterpret_cast<const float2*>(al)[h];
           u[s][h] = make_float2(o ? a.x : G[h].x, o ? a.y : G[h].y);  // UNWIND(s) folded into u
         }
+        if constexpr (kTail) ut[s] = o ? al[TQ] : Gt;
       }
     }
     int c = 0;
 #pragma unroll
     for (int i = 0; i < KM; ++i) {
       if (i < KM - 1 || i < k) {
-        float2 y[QH];
+        float2 y[NP > 0 ? NP : 1];
         const int cdiag = c++;
         float2 a = acc[cdiag];
 #pragma unroll
-        for (int h = 0; h < QH; ++h) {
+        for (int h = 0; h < NP; ++h) {
           y[h] = __fmul2_rn(W[h], u[i][h]);
           a = __ffma2_rn(y[h], make_float2(2.f, 2.f), a);  // phi_i = 2 sum_q W_q u_iq
+        }
+        float yt = 0.f;
+        if constexpr (kTail) {
+          yt = Wt * ut[i];
+          a.x = fmaf(yt, 2.f, a.x);
         }
 #pragma unroll
         for (int j = i + 1; j < KM; ++j) {
           if (j < KM - 1 || j < k) {
 #pragma unroll
-            for (int h = 0; h < QH; ++h) acc[c] = __ffma2_rn(y[h], u[j][h], acc[c]);
+            for (int h = 0; h < NP; ++h) acc[c] = __ffma2_rn(y[h], u[j][h], acc[c]);
+            if constexpr (kTail) acc[c].x = fmaf(yt, ut[j], acc[c].x);
           }
           ++c;
         }
@@ -778,14 +796,21 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
     const T* gam = gauss + (q - 1) * 3 * kQMax + 2 * kQMax;
     switch (q) {
       case 1: inter_run<T, 1, R, true>(k, n_run, E, tab, gam, xb, ab); break;
-      case 2: inter_run<T, 2, R, true>(k, n_run, E, tab, gam, xb, ab); break;
+      case 2:
+        if constexpr ((GTS_INTER_PAIRED & (1 << 2)) && sizeof(T) == 4 && R == 1) {
+          inter_run_q2<2>(k, n_run, E, reinterpret_cast<const float*>(tab), reinterpret_cast<const float*>(gam),
+                          xb, ab);
+        } else {
+          inter_run<T, 2, R, true>(k, n_run, E, tab, gam, xb, ab);
+        }
+        break;
       default:
 #pragma unroll 1
         for (int r = 0; r < R; ++r) {
           const int xb1[1] = {xb[r]}, ab1[1] = {ab[r]};
           switch (q) {
             case 3:
-              if constexpr (GTS_INTER_Q2 == 1 && sizeof(T) == 4) {
+              if constexpr ((GTS_INTER_PAIRED & (1 << 3)) && sizeof(T) == 4) {
                 inter_run_q2<3>(k, n_run, E, reinterpret_cast<const float*>(tab),
                                 reinterpret_cast<const float*>(gam), xb1, ab1);
               } else {
@@ -793,7 +818,7 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
               }
               break;
             case 4:
-              if constexpr (GTS_INTER_Q2 && sizeof(T) == 4) {
+              if constexpr ((GTS_INTER_PAIRED & (1 << 4)) && sizeof(T) == 4) {
                 inter_run_q2<4>(k, n_run, E, reinterpret_cast<const float*>(tab),
                                 reinterpret_cast<const float*>(gam), xb1, ab1);
               } else {
