@@ -495,7 +495,8 @@ def run_ours(args):
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         try:
-            tr = json.load(open(traffic_file)).get(f"{args.workload}/{args.layout}/{dominant}/{args.dtype}")
+            tr = json.load(open(traffic_file)).get(
+                f"{args.workload}/{args.layout}/{'both' if fused else dominant}/{args.dtype}")
             if tr:
                 roofline["traffic"] = tr.get("dram_bytes_per_launch")
                 roofline["traffic_source"] = tr.get("source")

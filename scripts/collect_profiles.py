@@ -3,7 +3,7 @@ the bench line, the ncu launch list with per-kernel shares, the ncu --set full
 summaries, test logs; and record per-launch DRAM traffic in profiles/traffic.json
 (read by bench.py for roofline.traffic).
 
-usage: python scripts/collect_profiles.py gpurun_out/r01a profiles/r01 [--key workload/layout/mode/dtype=kernelregex ...]
+usage: python scripts/collect_profiles.py gpurun_out/r01a profiles/r01 [workload/layout/mode/dtype=kernelregex[@capture] ...]
 """
 import collections
 import csv
@@ -74,6 +74,9 @@ def main():
         tr = rep_traffic(os.path.join(src, rep))
         rep = rep[:-8] + ".ncu-rep" if rep.endswith(".raw.csv") else rep
         for key, rx in keys:
+            rx, _, only = rx.partition("@")  # key=kernelregex@capture: only that capture's kernels
+            if only and not rep.startswith(only):
+                continue
             for kname, vals in tr.items():
                 if re.search(rx, kname) and vals and all(v == v for v in vals):
                     traffic[key] = {"dram_bytes_per_launch": sum(vals) / len(vals), "kernel": kname,

@@ -27,4 +27,7 @@ if [ "${NCU:-1}" = "1" ]; then
     OUT=$OUT NAME=nodal_$m WL=${WL:-cal_housing-med} ROWS=${NCU_ROWS:-1048576} MODE=$m KEEP=${KEEP:-0} bash scripts/ncu_one.sh
     head -24 $OUT/nodal_$m.summary.txt
   done
+  OUT=$OUT NAME=nodal_fused WL=${WL:-cal_housing-med} ROWS=${NCU_ROWS:-1048576} MODE=both SKIP=5 COUNT=1 KEEP=${KEEP:-0} \
+    bash scripts/ncu_one.sh
+  head -24 $OUT/nodal_fused.summary.txt
 fi

@@ -6,7 +6,9 @@ set -u
 OUT=${OUT:-gpurun_out/ncu}
 mkdir -p $OUT
 N=1; [ "${MODE:-both}" = "both" ] && N=2
-timeout ${NCU_TIMEOUT:-900} ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-nodal_kernel} -s $N -c $N \
+# mode both, warm-up 1: nodal launches are SHAP, interactions, fused (warm-up) then the same three timed;
+# SKIP=5 COUNT=1 captures the timed fused call
+timeout ${NCU_TIMEOUT:-900} ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-nodal_kernel} -s ${SKIP:-$N} -c ${COUNT:-$N} \
   -o $OUT/${NAME:-prof} python bench.py --workload ${WL:-cal_housing-med} --mode ${MODE:-both} --steps 1 --warmup 1 \
   --rows-per-gpu ${ROWS:-262144} --no-cpu-baseline --no-e2e --no-ablation ${BARGS:-} > $OUT/${NAME:-prof}.log 2>&1
 echo "ncu ${NAME:-prof} rc=$?"
