@@ -44,6 +44,12 @@
 #define GTS_X2_R2_QMAX 6  // largest Q whose paired-node SHAP run keeps both rows of a lane in flight
                           // (measured: adult SHAP +19 % for 6 over 4; profiles/r01h)
 #endif
+#ifndef GTS_SHAP_R_WIDE
+#define GTS_SHAP_R_WIDE 1  // rows per lane of the fp32 SHAP kernel with 32 or 64 slots
+#endif
+#ifndef GTS_SHAP_RECOMPUTE_O
+#define GTS_SHAP_RECOMPUTE_O 0  // scalar SHAP runs: recompute o_s for UNWIND instead of keeping o-bits
+#endif
 #ifndef GTS_SHAP_R8
 #define GTS_SHAP_R8 4  // rows per lane of the fp32 SHAP kernel with 8 slots (measured: 4 > 2)
 #endif
@@ -162,7 +168,10 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
         lds_vec(C, tp + NT * QP + s * NT * QP + QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          if ((om[r] >> s) & 1u) {
+          bool o;
+          if constexpr (GTS_SHAP_RECOMPUTE_O) o = one_fraction(xv[r][s], Ep[s]);
+          else o = (om[r] >> s) & 1u;
+          if (o) {
 #pragma unroll
             for (int q = 0; q < Q; ++q) acc[r][s] = fma(P[r][q], C[q], acc[r][s]);  // UNWIND(s) folded into C'
           }
@@ -879,7 +888,8 @@ template <typename T, bool kInter, int S>
 struct Cfg {
   static constexpr int R = (sizeof(T) == 4 && !kInter && S == 8) ? GTS_SHAP_R8
                            : (sizeof(T) == 4 && kInter && S == 8) ? GTS_INTER_R8
-                           : ((sizeof(T) == 4 && !kInter && S <= 16) ? 2 : 1);
+                           : ((sizeof(T) == 4 && !kInter && S <= 16) ? 2
+                              : ((sizeof(T) == 4 && !kInter) ? GTS_SHAP_R_WIDE : 1));
   static constexpr int tile_bytes = (int)sizeof(T) * tile_words_per_warp<T, S, R, kInter>();
   static constexpr int W = tile_bytes * 8 <= 74 * 1024 ? 8 : (tile_bytes * 4 <= 80 * 1024 ? 4 : 2);
   static constexpr int kMinBlocks = 2;
