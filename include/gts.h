@@ -238,7 +238,10 @@ gts_status gts_shap_and_interactions(const gts_blob_info* info, const void* d_bl
                                      void* stream);
 
 /* Number of kernel launches one call issues: interactions = 0 for gts_shap,
-   1 for gts_shap_interactions, 2 for gts_shap_and_interactions. */
+   1 for gts_shap_interactions, 2 for gts_shap_and_interactions.  NODAL blobs
+   with per-chunk slot maps (n_features > max_slots) add one pass to the
+   interaction calls: the kernel adds each pair to (i, j), i < j, only, and a
+   tiled transpose copies it to (j, i) (phi_ij is symmetric, Eq. 3). */
 int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions);
 
 const char* gts_last_error(void);

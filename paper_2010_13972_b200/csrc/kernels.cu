@@ -71,6 +71,45 @@ __global__ void init_phi_ij_kernel(T* __restrict__ phi, int64_t n_rows, int G, i
   }
 }
 
+// phi_ij is symmetric (Eq. 3).  With per-chunk slot maps (wide models) the
+// interaction kernel adds each pair once, to (i, j) with feature i < j (slot
+// maps are sorted), which halves its atomics; this pass then copies the upper
+// triangle of every [M+1][M+1] matrix onto the lower one through 32 x 32
+// shared-memory tiles (coalesced reads and writes).
+template <typename T>
+__global__ void mirror_kernel(T* __restrict__ phi, int64_t n_mats, int M1) {
+  __shared__ T tile[32][33];
+  const int nt = (M1 + 31) / 32;
+  const int64_t tiles_per_mat = (int64_t)nt * (nt + 1) / 2;
+  for (int64_t t = blockIdx.x; t < n_mats * tiles_per_mat; t += gridDim.x) {
+    const int64_t mat = t / tiles_per_mat;
+    const int tt = (int)(t - mat * tiles_per_mat);
+    int bi = 0;  // lower-triangle tile (bi, bj), bi >= bj
+    while ((bi + 1) * (bi + 2) / 2 <= tt) ++bi;
+    const int bj = tt - bi * (bi + 1) / 2;
+    T* m = phi + mat * (int64_t)M1 * M1;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+      const int a = bj * 32 + y, b = bi * 32 + threadIdx.x;  // upper source (a, b)
+      if (a < M1 && b < M1) tile[y][threadIdx.x] = m[(int64_t)a * M1 + b];
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+      const int b = bi * 32 + y, a = bj * 32 + threadIdx.x;  // lower target (b, a) = (a, b)
+      if (a < M1 && b < M1 && b > a) m[(int64_t)b * M1 + a] = tile[threadIdx.x][y];
+    }
+    __syncthreads();
+  }
+}
+
+#ifndef GTS_INTER_MIRROR
+#define GTS_INTER_MIRROR 1  // per-chunk slot maps: upper-triangle atomics + mirror pass
+#endif
+
+bool uses_mirror(const gts_blob_info* info) {
+  return GTS_INTER_MIRROR && info->layout == GTS_LAYOUT_NODAL && info->n_units > 0 &&
+         info->max_slots < info->n_features;
+}
+
 // ------------------------------------------------------------- launchers
 
 constexpr int64_t kBiasOffset = 256;  // align256(sizeof(BlobHeader)), host.cpp blob_plan
@@ -155,6 +194,7 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   a.col_stride = cs;
   a.out = out;
   a.out_phi = out_phi;
+  a.upper_only = kInter && uses_mirror(info);
   a.n_splits = (int)splits;
   a.M = info->n_features;
   a.G = info->n_groups;
@@ -164,7 +204,14 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   const int64_t blocks = row_tiles * splits;
   if (blocks > INT32_MAX) return fail(GTS_ERR_INVALID_ARGUMENT, "too many rows");
   kern<<<(unsigned)blocks, W * 32, smem, st>>>(a);
-  return cuda_check("nodal kernel launch");
+  gts_status s = cuda_check("nodal kernel launch");
+  if (s != GTS_OK || !a.upper_only) return s;
+  const int M1 = info->n_features + 1;
+  const int64_t nt = (M1 + 31) / 32;
+  const int64_t tiles = n_rows * info->n_groups * (nt * (nt + 1) / 2);
+  const int mblocks = (int)std::min<int64_t>(tiles, (int64_t)num_sms() * 16);
+  mirror_kernel<T><<<mblocks, dim3(32, 8), 0, st>>>(static_cast<T*>(out), n_rows * info->n_groups, M1);
+  return cuda_check("mirror kernel launch");
 }
 
 template <typename T, bool kInter>
@@ -313,9 +360,10 @@ gts_status gts_shap_and_interactions(const gts_blob_info* info, const void* d_bl
 int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions) {
   if (!info) return 0;
   const int32_t main = info->n_units > 0 ? 1 : 0;
+  const int32_t mirror = gts::uses_mirror(info) ? 1 : 0;
   if (interactions == 2)  // gts_shap_and_interactions
-    return info->layout == GTS_LAYOUT_NODAL ? 2 + main : 2 + 2 * main;
-  return 1 + main;  // init + main kernel
+    return info->layout == GTS_LAYOUT_NODAL ? 2 + main + mirror : 2 + 2 * main;
+  return 1 + main + (interactions ? mirror : 0);  // init + main kernel (+ mirror pass)
 }
 
 }  // extern "C"

@@ -868,6 +868,7 @@ struct Args {
   int64_t row_stride, col_stride;  // X[r][f] at X[r * row_stride + f * col_stride]
   void* out;
   void* out_phi;  // interaction kernel only: if set, the phi_i cells are also added to phi (fused call)
+  int upper_only;  // interaction kernel only: write cells (i, j) with i < j only; mirror_kernel fills (j, i)
   int n_splits;
   int M, G;
   int64_t n_chunks;
@@ -1032,7 +1033,7 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
               if (v != (T)0) {
                 const int fj = slotmap[cur_map_begin + j];
                 atomicAdd(base + (size_t)fi * M1 + fj, v);
-                atomicAdd(base + (size_t)fj * M1 + fi, v);
+                if (!a.upper_only) atomicAdd(base + (size_t)fj * M1 + fi, v);
               }
             }
           }
