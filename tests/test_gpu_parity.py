@@ -156,6 +156,23 @@ def test_fused_ragged_and_feature_major(gpu, layout):
                 parity.check(phi_ij.cpu().numpy(), oracle.interactions(ens, x64), "f32", f"n={n} fm={fm} ij")
 
 
+@pytest.mark.parametrize("name", ["fashion_mnist-med", "covtype-large"])
+def test_wide_interactions_mirror_symmetric(gpu, name):
+    """Per-chunk slot maps: the kernel writes (i, j), i < j, and the mirror pass
+    copies it to (j, i) over ragged 32 x 32 tiles (M+1 = 785 / 55): the result
+    is exactly symmetric for every row, and matches O6 on a sample."""
+    from paper_2010_13972_b200 import gts
+    w = WORKLOADS[name]
+    ens = w.ensemble().subset(range(60))
+    x = w.x(37, ens=ens)
+    ex = _explainer(ens, "f32")
+    assert ex.blob_int.info.max_slots < w.n_features
+    assert gts.gts_launches_per_call(ex.blob_int.info, True) == 3  # init + kernel + mirror
+    got = _run(ex, x, inter=True)
+    assert np.array_equal(got, np.swapaxes(got, 2, 3))
+    parity.check(got[:3], oracle.interactions(ens, x[:3].astype(np.float64)), "f32", f"{name} mirror")
+
+
 # ------------------------------------------------------------------ edges
 
 @pytest.mark.parametrize("layout", LAYOUTS)
