@@ -66,6 +66,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ablation", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-serial", action="store_true",
+                    help="e2e: one H2D, the call(s), one D2H, serialised (default: explain_host_pipelined)")
+    ap.add_argument("--e2e-chunks", type=int, default=4,
+                    help="row chunks of the pipelined e2e call (measured: 2 and 4 best, 3 and 8 lose to wave tails)")
     ap.add_argument("--separate", action="store_true",
                     help="mode both: time the step as gts_shap + gts_shap_interactions instead of the fused "
                          "gts_shap_and_interactions call")
@@ -373,7 +377,16 @@ def run_ours(args):
         phi_ij_h = torch.empty((e2e_chunk,) + tuple(phi_ij.shape[1:]), dtype=tdt, pin_memory=True) if do_int else None
         xe = torch.empty_like(xd)
 
+        pipelined = not args.e2e_serial and ij_chunk == n and args.x_layout == "row"
+        if pipelined:
+            phi_ij_h = torch.empty(tuple(phi_ij.shape), dtype=tdt, pin_memory=True) if do_int else None
+            del phi_ij  # the pipelined call has its own device slots
+            torch.cuda.empty_cache()
+
         def e2e_step():
+            if pipelined:
+                ex.explain_host_pipelined(x_pin, phi_h, phi_ij_h, chunk_rows=max(1, -(-n // args.e2e_chunks)))
+                return
             xe.copy_(x_pin, non_blocking=True)
             if fused:
                 for r0 in range(0, n, e2e_chunk):
@@ -408,9 +421,11 @@ def run_ours(args):
         d2h = (phi.numel() * phi.element_size() if do_shap else 0) + (n * ij_row_bytes if do_int else 0)
         e2e = {"value": world * n / (ms_e2e / 1000.0), "unit": "rows/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e,
-               "api": ("TreeShapExplainer.shap_and_interactions_device" if fused else
-                       "TreeShapExplainer.shap_device/interactions_device") +
-                      " with pinned host X and phi (H2D + D2H)"}
+               "api": (f"TreeShapExplainer.explain_host_pipelined (pinned host X -> {args.e2e_chunks} chunks on "
+                       "3 streams, H2D / kernel / D2H overlapped -> pinned host phi and phi_ij)" if pipelined else
+                       ("TreeShapExplainer.shap_and_interactions_device" if fused else
+                        "TreeShapExplainer.shap_device/interactions_device") +
+                       " with pinned host X and phi (H2D + D2H)")}
 
     # --- ablation: the paper-lineage warp-bin kernels on a slice of the rows
     ablation = None

@@ -140,6 +140,74 @@ class TreeShapExplainer:
                                       out_phi.data_ptr(), out_phi_ij.data_ptr(), st.cuda_stream)
         return out_phi, out_phi_ij
 
+    def explain_host_pipelined(self, X_host: torch.Tensor, phi_host: torch.Tensor | None = None,
+                               phi_ij_host: torch.Tensor | None = None, chunk_rows: int = 1 << 17):
+        """Host rows in, host outputs out, with the copies hidden behind the kernels.
+
+        X_host [n][M] and the outputs (phi_host [n][G][M+1] and/or phi_ij_host
+        [n][G][M+1][M+1]; None = not wanted, at least one given) should be pinned.  Rows go in
+        chunks through two device buffer slots on three streams: H2D of chunk
+        i+1 and D2H of chunk i-1 run while chunk i computes (gts_shap,
+        gts_shap_interactions or gts_shap_and_interactions, whichever the
+        outputs ask for).  Everything is ordered before the current stream,
+        so the caller synchronises (or records an event) as for any other call."""
+        n, M = X_host.shape
+        G, M1 = self.n_groups, self.n_features + 1
+        want_phi, want_ij = phi_host is not None, phi_ij_host is not None
+        if not (want_phi or want_ij):
+            raise ValueError("no output requested")
+        if n == 0:
+            return phi_host, phi_ij_host
+        cr = max(1, min(int(chunk_rows), n))
+        dev = self.device
+        main = torch.cuda.current_stream(dev)
+        if not hasattr(self, "_pipe_streams"):
+            self._pipe_streams = tuple(torch.cuda.Stream(dev) for _ in range(3))
+        hs, ks, ds = self._pipe_streams
+        for st in (hs, ks, ds):
+            st.wait_stream(main)
+        slots = []
+        for _ in range(min(2, -(-n // cr))):
+            slots.append((torch.empty((cr, M), dtype=self.torch_dtype, device=dev),
+                          torch.empty((cr, G, M1), dtype=self.torch_dtype, device=dev) if want_phi else None,
+                          torch.empty((cr, G, M1, M1), dtype=self.torch_dtype, device=dev) if want_ij else None))
+        ev_k = [None] * len(slots)
+        ev_d = [None] * len(slots)
+        for i, r0 in enumerate(range(0, n, cr)):
+            r1 = min(n, r0 + cr)
+            m = r1 - r0
+            b = i % len(slots)
+            xb, pb, qb = slots[b]
+            if ev_k[b] is not None:
+                hs.wait_event(ev_k[b])  # the kernel that read this slot's X is done
+            with torch.cuda.stream(hs):
+                xb[:m].copy_(X_host[r0:r1], non_blocking=True)
+                e_h = torch.cuda.Event()
+                e_h.record(hs)
+            ks.wait_event(e_h)
+            if ev_d[b] is not None:
+                ks.wait_event(ev_d[b])  # this slot's outputs have reached the host
+            with torch.cuda.stream(ks):
+                if want_phi and want_ij:
+                    self.shap_and_interactions_device(xb[:m], out_phi=pb[:m], out_phi_ij=qb[:m], stream=ks)
+                elif want_phi:
+                    self.shap_device(xb[:m], out=pb[:m], stream=ks)
+                else:
+                    self.interactions_device(xb[:m], out=qb[:m], stream=ks)
+                ev_k[b] = torch.cuda.Event()
+                ev_k[b].record(ks)
+            ds.wait_event(ev_k[b])
+            with torch.cuda.stream(ds):
+                if want_phi:
+                    phi_host[r0:r1].copy_(pb[:m], non_blocking=True)
+                if want_ij:
+                    phi_ij_host[r0:r1].copy_(qb[:m], non_blocking=True)
+                ev_d[b] = torch.cuda.Event()
+                ev_d[b].record(ds)
+        for st in (hs, ks, ds):
+            main.wait_stream(st)  # later work on the current stream (incl. reuse of the slots) waits
+        return phi_host, phi_ij_host
+
     def graphed(self, n_rows: int, interactions: bool = False) -> "GraphedCall":
         """Latency regime: capture one call for
         a fixed row count into a CUDA graph over static X / output buffers, so
