@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define GTS_ABI_VERSION 2  /* 2: blob element records {lo, hi, slot, tri}, C' tables, 2-table blobs above 16 slots */
+#define GTS_ABI_VERSION 3  /* 3: blob uses (SHAP / interactions) recorded in the info; 32-slot interaction blobs */
 #define GTS_WARP_CAPACITY 32 /* lanes per warp = bin capacity B */
 
 typedef enum gts_status {
@@ -53,7 +53,7 @@ typedef enum gts_status {
                                    cover <= 0, cover(parent) != cover(l)+cover(r) beyond 1e-6
                                    relative, non-finite threshold / value, bad group */
   GTS_ERR_PATH_TOO_LONG = 3,    /* merged path length (root included) > 32 */
-  GTS_ERR_NONFINITE = 4,        /* reserved: non-finite X when validation is requested */
+  GTS_ERR_NONFINITE = 4,        /* non-finite X found by gts_validate_x (reading G17) */
   GTS_ERR_CUDA = 5,             /* CUDA launch / runtime error */
   GTS_ERR_OUT_OF_MEMORY = 6     /* host allocation failed */
 } gts_status;
@@ -178,15 +178,42 @@ typedef struct gts_blob_info {
   int64_t max_chunk_bytes;      /* NODAL: staged bytes of the largest chunk (shared memory) */
   int64_t max_chunk_elems;
   int64_t max_chunk_paths;
-  int64_t reserved[5];
+  int32_t uses;                 /* gts_blob_use bits the blob serves (NODAL; WARP_BINS: both) */
+  int32_t n_tables;             /* NODAL: nodal table rows per element record (2 or 3) */
+  int64_t reserved[4];
 } gts_blob_info;
 
+/* What a blob is planned for.  NODAL blobs carry per-path nodal tables
+   (blob_format.h); the SHAP kernel needs {rho, C'} per element, the
+   interaction kernel {rho, alpha} plus the per-path h row, and its shared
+   memory tile holds S(S+1)/2 pair cells per row, so it takes S <= 32 slots. */
+typedef enum gts_blob_use {
+  GTS_USE_SHAP = 1,
+  GTS_USE_INTERACTIONS = 2,
+  GTS_USE_BOTH = 3
+} gts_blob_use;
+
 /* Describe the blob for (bins, dtype, layout).  max_slots (NODAL only) is the
-   number of distinct features a chunk may touch, one of 16, 32, 64, or 0 for
-   the default (the smallest of them >= n_features, else 32).  Interactions
-   need max_slots <= 16 (shared-memory tile).  Errors: INVALID_ARGUMENT. */
+   number of distinct features a chunk may touch, one of 8, 16, 32, 64, or 0
+   for the default (the smallest of them >= n_features, raised to the longest
+   merged path; above 64 features, 32 with per-chunk slot maps).  The blob
+   serves gts_shap, and the interaction calls too when its slot width is <= 16
+   (uses = GTS_USE_BOTH; otherwise GTS_USE_SHAP).  Errors: INVALID_ARGUMENT. */
 gts_status gts_blob_plan(const gts_bins* bins, gts_dtype dtype, gts_layout layout, int32_t max_slots,
                          gts_blob_info* info);
+/* Same, for an explicit use.  NODAL with GTS_USE_INTERACTIONS (or BOTH):
+   max_slots one of 8, 16, 32 or 0 = default (8 when n_features <= 8, else 16,
+   raised to 32 when a merged path has more than 16 features -- the paper's
+   bound is 31); every such blob serves the interaction
+   calls and gts_shap_and_interactions, and gts_shap too when uses is
+   GTS_USE_BOTH, which needs a slot width <= 16 (the SHAP kernel reads
+   2-row tables above 16 slots).  GTS_USE_SHAP is gts_blob_plan's SHAP
+   layout.  WARP_BINS blobs serve every call (uses = BOTH whatever is asked).
+   Errors: INVALID_ARGUMENT (bad use, slot width smaller than the longest
+   merged path on a per-chunk slot map, interaction slot width > 32, BOTH
+   above 16 slots). */
+gts_status gts_blob_plan_for(const gts_bins* bins, gts_dtype dtype, gts_layout layout, int32_t max_slots,
+                             gts_blob_use uses, gts_blob_info* info);
 /* Serialise into caller HOST memory of at least info->bytes (any alignment
    >= 16).  The caller copies the bytes to a device buffer (16-byte aligned). */
 gts_status gts_blob_write(const gts_bins* bins, const gts_blob_info* info, void* host_dst, size_t dst_bytes);
@@ -206,7 +233,8 @@ gts_status gts_shap(const gts_blob_info* info, const void* d_blob, const void* d
 /* SHAP interaction values; d_phi_ij: device
    [n_rows][n_groups][n_features+1][n_features+1] of info->dtype, fully
    overwritten: off-diagonal Eq. 3, diagonal Eq. 6, cell (M,M) = bias,
-   cells (i,M) and (M,i) = 0.  NODAL blobs need max_slots <= 16. */
+   cells (i,M) and (M,i) = 0.  NODAL blobs need uses & GTS_USE_INTERACTIONS
+   (checked before any launch; gts_shap likewise needs GTS_USE_SHAP). */
 gts_status gts_shap_interactions(const gts_blob_info* info, const void* d_blob, const void* d_X,
                                  int64_t n_rows, int64_t ld_x, void* d_phi_ij, void* stream);
 
@@ -236,6 +264,17 @@ gts_status gts_shap_interactions_strided(const gts_blob_info* info, const void* 
 gts_status gts_shap_and_interactions(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
                                      int64_t row_stride, int64_t col_stride, void* d_phi, void* d_phi_ij,
                                      void* stream);
+
+/* Optional validation of X (reading G17: the method is defined for finite
+   inputs only; PAPER.md:50 covers absent features, not NaN).  Checks every
+   entry (r, f), f < n_features, of a row- or feature-major X as above on
+   `stream` and SYNCHRONISES the stream: GTS_ERR_NONFINITE (message names the
+   first offending entry in row-major order) if any is NaN or +-inf, GTS_OK
+   otherwise.  The compute calls never check (it costs a pass over X and a
+   host sync); callers that cannot vouch for X call this first.  Errors:
+   INVALID_ARGUMENT, CUDA, NONFINITE. */
+gts_status gts_validate_x(gts_dtype dtype, const void* d_X, int64_t n_rows, int32_t n_features, int64_t row_stride,
+                          int64_t col_stride, void* stream);
 
 /* Number of kernel launches one call issues: interactions = 0 for gts_shap,
    1 for gts_shap_interactions, 2 for gts_shap_and_interactions.  NODAL blobs

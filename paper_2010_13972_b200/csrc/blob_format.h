@@ -37,7 +37,9 @@ struct BlobHeader {            // 256 bytes at offset 0
   int64_t max_chunk_bytes;     // NODAL: largest staged region of any chunk
   int64_t max_chunk_elems;     // NODAL: largest element count of any chunk
   int64_t max_chunk_paths;
-  int64_t reserved[12];
+  int32_t uses;                // gts_blob_use bits (NODAL: which kernels the tables serve)
+  int32_t n_tables;            // NODAL: table rows per record (2: SHAP only; 3: interactions)
+  int64_t reserved[11];
 };
 static_assert(sizeof(BlobHeader) == 256, "header size");
 
@@ -63,25 +65,19 @@ struct ChunkRec {              // 64 bytes
 };
 static_assert(sizeof(ChunkRec) == 64, "chunk size");
 
-// host-side planning records (not stored in the blob)
+// host-side planning record (not stored in the blob)
 struct PathRec {
   int32_t k;                   // non-root merged elements (1..31) | run length << 16 (run heads only):
                                // a run = consecutive paths of a chunk with one feature set
   int32_t q;                   // Gauss nodes: ceil(k/2)
   int32_t elem;                // first element, relative to the chunk
   int32_t table;               // first word of the path's table, relative to the chunk's tables
-  double v;                    // leaf value
+  int64_t src;                 // index of the path in the canonical table (gts_paths)
 };
 
-struct ElemRec {
-  int32_t slot;                // feature slot within the chunk's slot map
-  float lo, hi;                // lo <= x < hi  <=> o = 1
-  int32_t pad;
-  double z;                    // merged zero fraction
-};
-
-// Nodal table of one path (T words, shared memory; NT = nodal_tables(S) rows
-// per record, the third row only when NT = 3).  Every row is padded to
+// Nodal table of one path (T words, shared memory; NT rows per record, the
+// third row only when NT = 3; interaction blobs always have NT = 3, SHAP-only
+// blobs NT = nodal_tables(S)).  Every row is padded to
 // QP = round_up(Q, 4) words (16-byte vector loads).  With A_sq = z_s + (1-z_s) t_q,
 // B_sq = z_s (1 - t_q) (f_s(t_q) for o_s = 1 / 0):
 //   c[QP]  prod_s A_sq                  (P(t_q) when every o = 1)

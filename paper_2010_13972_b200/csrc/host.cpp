@@ -12,6 +12,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <set>
 #include <string>
@@ -62,8 +63,14 @@ struct gts_paths {
   std::shared_ptr<gts::PathTable> tab;
 };
 
+namespace gts {
+struct PlanCache;
+}
+
 struct gts_bins {
   std::shared_ptr<gts::PathTable> tab;
+  mutable std::mutex cache_mu;                   // guards cache
+  mutable std::shared_ptr<gts::PlanCache> cache;  // last blob plan, taken by gts_blob_write
   int32_t capacity = 32;
   int32_t algo = 0;
   int64_t n_bins = 0;
@@ -456,11 +463,12 @@ struct NodalPlan {
   std::vector<ChunkRec> chunks;
   std::vector<int32_t> slotmap;
   std::vector<PathRec> paths;
-  std::vector<ElemRec> elems;
+  std::vector<uint8_t> slots;  // slot of every planned element, chunk after chunk
   std::vector<double> work_shap, work_inter;
   int64_t max_words = 0, max_elems = 0, max_paths = 0;
 };
 
+// Default slot width of a SHAP-only blob: identity slot map up to 64 features.
 static int pick_slots(int32_t requested, int32_t M) {
   if (requested != 0) return requested;
   if (M <= 8) return 8;
@@ -479,56 +487,81 @@ static double nodal_inter_flops(int k, int q) {
 static double paper_shap_flops(int k) { return 5.5 * k * k + 7.5 * k; }
 static double paper_inter_flops(int k) { return paper_shap_flops(k) + (double)k * (k - 1) * (5.5 * k + 1) + 2.0 * k; }
 
-static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np) {
+// Chunking (blob_format.h): consecutive paths of one group, at most kChunkBytes
+// of staged records + tables, at most S distinct features.  With an identity
+// slot map (M <= S) the paths of a group are first ordered by (Q descending,
+// length descending, feature set, index) so that paths sharing a feature set
+// form runs; the feature set of a path is its bit mask (M <= 64).  Per-chunk
+// slot maps (wide models) keep the input (DFS) order, which keeps the features
+// of consecutive paths local.
+static void plan_nodal(const PathTable& tab, int S, int nt, size_t tsize, NodalPlan& np) {
   const int32_t M = tab.n_features;
   const bool identity = M <= S;
   const int64_t L = tab.n_paths();
-  // Paths grouped by group.  Within a group: for identity slot maps, ordered by
-  // (Q descending, feature set, index) so that paths sharing a feature set form
-  // long runs; for per-chunk maps (wide models), input (DFS) order, which keeps
-  // the features of consecutive paths local.
+  std::vector<uint64_t> mask;
+  if (identity) {
+    mask.assign(L, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < L; ++p) {
+      uint64_t m = 0;
+      for (int64_t e = tab.path_offset[p] + 1; e < tab.path_offset[p + 1]; ++e) m |= 1ull << tab.feature[e];
+      mask[p] = m;
+    }
+  }
   auto fs_less = [&](int64_t a, int64_t b) {
-    const int qa = tab.len(a) / 2, qb = tab.len(b) / 2;
-    if (qa != qb) return qa > qb;
     const int la = tab.len(a), lb = tab.len(b);
+    const int qa = la / 2, qb = lb / 2;
+    if (qa != qb) return qa > qb;
     if (la != lb) return la > lb;
-    for (int i = 1; i < la; ++i) {
-      const int32_t fa = tab.feature[tab.path_offset[a] + i], fb = tab.feature[tab.path_offset[b] + i];
-      if (fa != fb) return fa < fb;
+    if (identity) {
+      if (mask[a] != mask[b]) return mask[a] < mask[b];
+    } else {
+      for (int i = 1; i < la; ++i) {
+        const int32_t fa = tab.feature[tab.path_offset[a] + i], fb = tab.feature[tab.path_offset[b] + i];
+        if (fa != fb) return fa < fb;
+      }
     }
     return a < b;
   };
   auto same_set = [&](int64_t a, int64_t b) {
     if (tab.len(a) != tab.len(b)) return false;
+    if (identity) return mask[a] == mask[b];
     for (int i = 1; i < tab.len(a); ++i)
       if (tab.feature[tab.path_offset[a] + i] != tab.feature[tab.path_offset[b] + i]) return false;
     return true;
   };
+  std::vector<std::vector<int64_t>> by_group(tab.n_groups);
+  for (int64_t p = 0; p < L; ++p)
+    if (tab.len(p) > 1) by_group[tab.group[p]].push_back(p);
+  if (identity) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t g = 0; g < tab.n_groups; ++g) std::sort(by_group[g].begin(), by_group[g].end(), fs_less);
+  }
   std::vector<int64_t> order;
   order.reserve(L);
-  for (int32_t g = 0; g < tab.n_groups; ++g) {
-    const size_t first = order.size();
-    for (int64_t p = 0; p < L; ++p)
-      if (tab.group[p] == g && tab.len(p) > 1) order.push_back(p);
-    if (identity) std::sort(order.begin() + first, order.end(), fs_less);
+  for (auto& v : by_group) {
+    order.insert(order.end(), v.begin(), v.end());
+    std::vector<int64_t>().swap(v);
   }
   // (Cutting small models into ~one chunk per SM lowered the 1-row latency of
   // cal_housing-small from 23 to 18 us but cost 30 % at 2^20 rows, since runs
   // and staging get shorter; profiles/r01h.  Not adopted.)
   const int chunk_paths = kMaxChunkPaths;
   // staged bytes of a chunk: element records + path headers (16 B each) + tables
-  const int nt = nodal_tables(S);
   auto path_bytes = [&](int k, int q) { return (int64_t)16 * (k + 1) + (int64_t)tsize * nodal_path_words(k, q, nt); };
   int32_t map_id = -1;
-  std::vector<int32_t> cur_map;  // sorted features of the current chunk (non-identity)
+  int32_t cur_map[64];
+  int n_cur = 0;
+  int32_t feats[64], u[128];
+  std::vector<int64_t> members;
   size_t i = 0;
   while (i < order.size()) {
     ChunkRec c{};
     c.group = tab.group[order[i]];
     c.path_begin = (int64_t)np.paths.size();
-    c.elem_begin = (int64_t)np.elems.size();
-    std::vector<int32_t> feats;
-    std::vector<int64_t> members;
+    c.elem_begin = (int64_t)np.slots.size();
+    int nf = 0;
+    members.clear();
     int64_t bytes = 0, nel = 0;
     size_t j = i;
     while (j < order.size() && (int)members.size() < chunk_paths) {
@@ -537,13 +570,19 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
       const int k = tab.len(p) - 1, q = (k + 1) / 2;
       const int64_t w = path_bytes(k, q);
       if (!members.empty() && bytes + w > kChunkBytes) break;
-      if (!identity) {
-        std::vector<int32_t> u = feats;
-        for (int64_t e = tab.path_offset[p] + 1; e < tab.path_offset[p + 1]; ++e) u.push_back(tab.feature[e]);
-        std::sort(u.begin(), u.end());
-        u.erase(std::unique(u.begin(), u.end()), u.end());
-        if (!members.empty() && (int)u.size() > S) break;
-        feats.swap(u);
+      if (!identity) {  // union of two sorted feature lists
+        const int32_t* pf = &tab.feature[tab.path_offset[p] + 1];
+        int a = 0, b = 0, n = 0;
+        while (a < nf || b < k) {
+          int32_t x;
+          if (b >= k || (a < nf && feats[a] < pf[b])) x = feats[a++];
+          else if (a >= nf || pf[b] < feats[a]) x = pf[b++];
+          else { x = feats[a++]; ++b; }
+          u[n++] = x;
+        }
+        if (!members.empty() && n > S) break;
+        std::memcpy(feats, u, sizeof(int32_t) * n);
+        nf = n;
       }
       members.push_back(p);
       bytes += w;
@@ -551,21 +590,22 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
       ++j;
     }
     if (identity) {
-      feats.resize(M);
+      nf = M;
       for (int32_t f = 0; f < M; ++f) feats[f] = f;
     }
     // inside the chunk: Q descending (template locality), then feature set (runs)
     std::sort(members.begin(), members.end(), fs_less);
-    if (feats != cur_map || map_id < 0) {
+    if (map_id < 0 || nf != n_cur || std::memcmp(feats, cur_map, sizeof(int32_t) * nf) != 0) {
       ++map_id;
-      cur_map = feats;
+      n_cur = nf;
+      std::memcpy(cur_map, feats, sizeof(int32_t) * nf);
       c.slotmap_begin = (int64_t)np.slotmap.size();
-      np.slotmap.insert(np.slotmap.end(), feats.begin(), feats.end());
+      np.slotmap.insert(np.slotmap.end(), feats, feats + nf);
     } else {
       c.slotmap_begin = np.chunks.back().slotmap_begin;
     }
     c.map_id = map_id;
-    c.n_slots = (int32_t)feats.size();
+    c.n_slots = (int32_t)nf;
     c.n_paths = (int32_t)members.size();
     c.n_elems = (int32_t)nel;
     int32_t table = 0, rel = 0, maxq = 0;
@@ -583,16 +623,11 @@ static void plan_nodal(const PathTable& tab, int S, size_t tsize, NodalPlan& np)
       pr.q = q;
       pr.elem = rel;
       pr.table = table;
-      pr.v = tab.v[p];
+      pr.src = p;
       np.paths.push_back(pr);
       for (int64_t e = tab.path_offset[p] + 1; e < tab.path_offset[p + 1]; ++e) {
-        ElemRec er{};
         const int32_t f = tab.feature[e];
-        er.slot = (int32_t)(std::lower_bound(feats.begin(), feats.end(), f) - feats.begin());
-        er.lo = tab.lower[e];
-        er.hi = tab.upper[e];
-        er.z = tab.zero_fraction[e];
-        np.elems.push_back(er);
+        np.slots.push_back((uint8_t)(identity ? f : (std::lower_bound(feats, feats + nf, f) - feats)));
       }
       rel += k;
       table += nodal_path_words(k, q, nt);
@@ -631,14 +666,55 @@ static void plan_bins(const gts_bins& b, BinsPlan& bp) {
   for (int64_t i = 0; i < b.n_bins; ++i) bp.kmax[i] = km[bp.bin_order[i]];
 }
 
-static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, int32_t max_slots,
+// Slot width and table rows of a NODAL blob for the requested uses.
+// uses == 0: gts_blob_plan's default (SHAP layout; interactions too when S <= 16).
+static gts_status nodal_shape(const PathTable& tab, int32_t max_slots, int32_t uses, int* S_out, int* nt_out,
+                              int32_t* uses_out) {
+  const int max_k = std::max(tab.max_len - 1, 0);
+  const int32_t M = tab.n_features;
+  int S;
+  if (uses == 0 || uses == GTS_USE_SHAP) {
+    if (max_slots != 0 && max_slots != 8 && max_slots != 16 && max_slots != 32 && max_slots != 64)
+      return fail(GTS_ERR_INVALID_ARGUMENT, "max_slots must be 0, 8, 16, 32 or 64");
+    S = pick_slots(max_slots, M);
+    if (max_slots == 0) {
+      while (S < max_k && S < 64) S *= 2;
+    } else if (S < max_k && S < M) {
+      return fail(GTS_ERR_INVALID_ARGUMENT,
+                  "max_slots %d is smaller than the %d features of the longest path", S, max_k);
+    }
+    *nt_out = nodal_tables(S);
+    *uses_out = uses == 0 ? (S <= 16 ? GTS_USE_BOTH : GTS_USE_SHAP) : GTS_USE_SHAP;
+  } else if (uses == GTS_USE_INTERACTIONS || uses == GTS_USE_BOTH) {
+    if (max_slots != 0 && max_slots != 8 && max_slots != 16 && max_slots != 32)
+      return fail(GTS_ERR_INVALID_ARGUMENT, "interaction blobs take max_slots 0, 8, 16 or 32 (got %d)", max_slots);
+    S = max_slots != 0 ? max_slots : (M <= 8 ? 8 : 16);
+    if (max_slots == 0) {
+      while (S < max_k) S *= 2;  // merged paths of 17..31 features: 32 slots
+    } else if (S < max_k && S < M) {
+      return fail(GTS_ERR_INVALID_ARGUMENT,
+                  "max_slots %d is smaller than the %d features of the longest path", S, max_k);
+    }
+    if (uses == GTS_USE_BOTH && S > 16)
+      return fail(GTS_ERR_INVALID_ARGUMENT,
+                  "GTS_USE_BOTH needs a slot width <= 16 (this model needs %d): plan a SHAP blob and an "
+                  "interaction blob", S);
+    *nt_out = 3;
+    *uses_out = uses;
+  } else {
+    return fail(GTS_ERR_INVALID_ARGUMENT, "bad blob uses %d", uses);
+  }
+  *S_out = S;
+  return GTS_OK;
+}
+
+static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, int32_t max_slots, int32_t uses,
                             gts_blob_info* info, BlobHeader* hdr, NodalPlan* np, BinsPlan* bp) {
   if (!b || !info) return fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
   if (dtype != GTS_F32 && dtype != GTS_F64) return fail(GTS_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
   if (layout != GTS_LAYOUT_NODAL && layout != GTS_LAYOUT_WARP_BINS)
     return fail(GTS_ERR_INVALID_ARGUMENT, "bad layout %d", layout);
-  if (max_slots != 0 && max_slots != 8 && max_slots != 16 && max_slots != 32 && max_slots != 64)
-    return fail(GTS_ERR_INVALID_ARGUMENT, "max_slots must be 0, 8, 16, 32 or 64");
+  if (uses < 0 || uses > GTS_USE_BOTH) return fail(GTS_ERR_INVALID_ARGUMENT, "bad blob uses %d", uses);
   const PathTable& tab = *b->tab;
   const size_t tsize = dtype == GTS_F32 ? 4 : 8;
   BlobHeader h{};
@@ -664,21 +740,19 @@ static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, in
     pi += paper_inter_flops(k);
   }
   if (layout == GTS_LAYOUT_NODAL) {
-    int S = pick_slots(max_slots, tab.n_features);
-    const int max_k = std::max(tab.max_len - 1, 0);
-    if (max_slots == 0) {
-      while (S < max_k && S < 64) S *= 2;
-    } else if (S < max_k && S < tab.n_features) {
-      return fail(GTS_ERR_INVALID_ARGUMENT,
-                  "max_slots %d is smaller than the %d features of the longest path", S, max_k);
-    }
+    int S = 0, nt = 0;
+    int32_t u = 0;
+    gts_status st = nodal_shape(tab, max_slots, uses, &S, &nt, &u);
+    if (st != GTS_OK) return st;
     h.max_slots = S;
+    h.uses = u;
+    h.n_tables = nt;
     NodalPlan local;
     NodalPlan& P = np ? *np : local;
-    plan_nodal(tab, S, tsize, P);
+    plan_nodal(tab, S, nt, tsize, P);
     h.n_units = (int64_t)P.chunks.size();
     h.n_kept_paths = (int64_t)P.paths.size();
-    h.n_kept_elems = (int64_t)P.elems.size();
+    h.n_kept_elems = (int64_t)P.slots.size();
     h.max_chunk_bytes = P.max_words;
     h.max_chunk_elems = P.max_elems;
     h.max_chunk_paths = P.max_paths;
@@ -698,6 +772,8 @@ static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, in
     off = align256(off);
   } else {
     h.max_slots = 0;
+    h.uses = GTS_USE_BOTH;
+    h.n_tables = 0;
     h.n_units = b->n_bins;
     if (b->capacity != kWarp)
       return fail(GTS_ERR_INVALID_ARGUMENT, "WARP_BINS layout needs capacity %d packing", kWarp);
@@ -731,6 +807,8 @@ static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, in
   info->max_chunk_bytes = h.max_chunk_bytes;
   info->max_chunk_elems = h.max_chunk_elems;
   info->max_chunk_paths = h.max_chunk_paths;
+  info->uses = h.uses;
+  info->n_tables = h.n_tables;
   if (hdr) *hdr = h;
   return GTS_OK;
 }
@@ -751,13 +829,21 @@ static void write_gauss(char* dst) {
 }
 
 // Staged chunk regions (blob_format.h): element records, path headers, and the
-// nodal tables, computed in long double from the fp64 zero fractions and leaf
-// values and rounded once to T (reading G11: one rounding in fp32 mode).
+// nodal tables, computed in fp64 from the fp64 zero fractions and leaf values
+// and rounded once to T (reading G11: one rounding in fp32 mode).  Per node the
+// reciprocals 1/A_sq and 1/(1 - t_q) are formed once and multiplied.
 template <typename T>
-static void write_regions(const NodalPlan& np, int S, char* out) {
-  long double tq[kQMax + 1][kQMax], wq[kQMax + 1][kQMax];
-  for (int Q = 1; Q <= kQMax; ++Q) gauss_legendre01(Q, tq[Q], wq[Q]);
-  const int nt = nodal_tables(S);
+static void write_regions(const PathTable& tab, const NodalPlan& np, int S, int nt, char* out) {
+  double tq[kQMax + 1][kQMax], wq[kQMax + 1][kQMax], rq[kQMax + 1][kQMax];
+  for (int Q = 1; Q <= kQMax; ++Q) {
+    long double t[kQMax], w[kQMax];
+    gauss_legendre01(Q, t, w);
+    for (int q = 0; q < Q; ++q) {
+      tq[Q][q] = (double)t[q];
+      wq[Q][q] = (double)w[q];
+      rq[Q][q] = (double)(1.0L / (1.0L - t[q]));
+    }
+  }
   const int64_t C = (int64_t)np.chunks.size();
 #pragma omp parallel for schedule(dynamic, 16)
   for (int64_t ci = 0; ci < C; ++ci) {
@@ -765,17 +851,7 @@ static void write_regions(const NodalPlan& np, int S, char* out) {
     char* region = out + c.data_off;
     int32_t* E = reinterpret_cast<int32_t*>(region);
     int32_t* Pp = E + 4 * (int64_t)c.n_elems;
-    T* tab = reinterpret_cast<T*>(Pp + 4 * (int64_t)c.n_paths);
-    for (int32_t e = 0; e < c.n_elems; ++e) {
-      const ElemRec& er = np.elems[c.elem_begin + e];
-      int32_t lo, hi;
-      std::memcpy(&lo, &er.lo, 4);
-      std::memcpy(&hi, &er.hi, 4);
-      E[4 * e + 0] = lo;
-      E[4 * e + 1] = hi;
-      E[4 * e + 2] = er.slot;
-      E[4 * e + 3] = er.slot * (2 * S - er.slot - 1) / 2;  // upper-triangle row base of the slot
-    }
+    T* tab_out = reinterpret_cast<T*>(Pp + 4 * (int64_t)c.n_paths);
     for (int32_t p = 0; p < c.n_paths; ++p) {
       const PathRec& pr = np.paths[c.path_begin + p];
       Pp[4 * p + 0] = pr.k;
@@ -783,23 +859,32 @@ static void write_regions(const NodalPlan& np, int S, char* out) {
       Pp[4 * p + 2] = pr.elem;
       Pp[4 * p + 3] = pr.table;
       const int k = pr.k & 0xff, Q = pr.q, QP = nodal_qp(Q);
-      const ElemRec* el = &np.elems[c.elem_begin + pr.elem];
-      T* t = tab + pr.table;
-      const long double v = pr.v;
+      const int64_t e0 = tab.path_offset[pr.src] + 1;  // first non-root element
+      const uint8_t* sl = &np.slots[c.elem_begin + pr.elem];
+      for (int s = 0; s < k; ++s) {
+        int32_t* rec = E + 4 * (int64_t)(pr.elem + s);
+        std::memcpy(&rec[0], &tab.lower[e0 + s], 4);
+        std::memcpy(&rec[1], &tab.upper[e0 + s], 4);
+        rec[2] = sl[s];
+        rec[3] = sl[s] * (2 * S - sl[s] - 1) / 2;  // upper-triangle row base of the slot
+      }
+      const double* z = &tab.zero_fraction[e0];
+      const double v = tab.v[pr.src];
+      T* t = tab_out + pr.table;
       for (int q = 0; q < Q; ++q) {
-        const long double tt = tq[Q][q], w = wq[Q][q];
-        long double cq = 1.0L;
-        for (int s = 0; s < k; ++s) cq *= (long double)el[s].z + (1.0L - el[s].z) * tt;
+        const double tt = tq[Q][q], w = wq[Q][q], r1 = rq[Q][q];
+        double cq = 1.0;
+        for (int s = 0; s < k; ++s) cq *= z[s] + (1.0 - z[s]) * tt;
         t[q] = (T)cq;
-        t[QP + q] = (T)(-v * w / (1.0L - tt));
-        if (nt == 3) t[2 * QP + q] = (T)(0.5L * v * w);
+        t[QP + q] = (T)(-v * w * r1);
+        if (nt == 3) t[2 * QP + q] = (T)(0.5 * v * w);
         for (int s = 0; s < k; ++s) {
-          const long double z = el[s].z;
-          const long double A = z + (1.0L - z) * tt, B = z * (1.0L - tt);
+          const double zs = z[s];
+          const double A = zs + (1.0 - zs) * tt, iA = 1.0 / A;
           T* row = t + nt * QP + s * nt * QP;
-          row[q] = (T)(B / A);
-          row[QP + q] = (T)(v * w * ((1.0L - z) / A + 1.0L / (1.0L - tt)));  // C' = C - d
-          if (nt == 3) row[2 * QP + q] = (T)((1.0L - z) / A);
+          row[q] = (T)(zs * (1.0 - tt) * iA);                 // rho = B / A
+          row[QP + q] = (T)(v * w * ((1.0 - zs) * iA + r1));  // C' = C - d
+          if (nt == 3) row[2 * QP + q] = (T)((1.0 - zs) * iA);
         }
       }
     }
@@ -849,16 +934,52 @@ static void write_bins(const gts_bins& b, const BinsPlan& bp, const BlobHeader& 
   }
 }
 
-static gts_status blob_write(const gts_bins* b, const gts_blob_info* info, void* dst, size_t dst_bytes) {
-  if (!b || !info || !dst) return fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
-  BlobHeader h;
+// The plan of the last gts_blob_plan* call on these bins is kept (keyed by its
+// arguments) for the gts_blob_write that normally follows, which takes it.
+struct PlanCache {
+  int32_t dtype = -1, layout = -1, max_slots = -1, uses = -1;
+  gts_blob_info info{};
+  BlobHeader hdr{};
   NodalPlan np;
   BinsPlan bp;
-  gts_blob_info fresh;
-  gts_status st = blob_plan(b, info->dtype, info->layout, info->max_slots, &fresh, &h, &np, &bp);
+};
+
+static gts_status blob_plan_cached(const gts_bins* b, int32_t dtype, int32_t layout, int32_t max_slots, int32_t uses,
+                                   gts_blob_info* info) {
+  if (!b || !info) return fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
+  auto pc = std::make_shared<PlanCache>();
+  gts_status st = blob_plan(b, dtype, layout, max_slots, uses, info, &pc->hdr, &pc->np, &pc->bp);
   if (st != GTS_OK) return st;
-  if (fresh.bytes != info->bytes || fresh.n_units != info->n_units)
-    return fail(GTS_ERR_INVALID_ARGUMENT, "blob info does not match these bins");
+  pc->dtype = dtype;
+  pc->layout = layout;
+  pc->max_slots = max_slots;
+  pc->uses = uses;
+  pc->info = *info;
+  std::lock_guard<std::mutex> lock(b->cache_mu);
+  b->cache = std::move(pc);
+  return GTS_OK;
+}
+
+static gts_status blob_write(const gts_bins* b, const gts_blob_info* info, void* dst, size_t dst_bytes) {
+  if (!b || !info || !dst) return fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (info->magic != kMagic || info->abi_version != GTS_ABI_VERSION)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "info is not a gts_blob_info of ABI version %d", GTS_ABI_VERSION);
+  std::shared_ptr<PlanCache> pc;
+  {
+    std::lock_guard<std::mutex> lock(b->cache_mu);
+    if (b->cache && std::memcmp(&b->cache->info, info, sizeof(*info)) == 0) pc = std::move(b->cache);
+  }
+  if (!pc) {  // re-plan: the blob's shape is a pure function of (bins, dtype, layout, slots, uses)
+    pc = std::make_shared<PlanCache>();
+    gts_blob_info fresh;
+    const int32_t req_uses = info->layout == GTS_LAYOUT_NODAL ? info->uses : 0;
+    gts_status st = blob_plan(b, info->dtype, info->layout, info->max_slots, req_uses, &fresh, &pc->hdr, &pc->np,
+                              &pc->bp);
+    if (st != GTS_OK) return st;
+    if (fresh.bytes != info->bytes || fresh.n_units != info->n_units || fresh.n_tables != info->n_tables)
+      return fail(GTS_ERR_INVALID_ARGUMENT, "blob info does not match these bins");
+  }
+  const BlobHeader& h = pc->hdr;
   if (dst_bytes < (size_t)h.bytes)
     return fail(GTS_ERR_INVALID_ARGUMENT, "destination too small: %zu < %lld", dst_bytes, (long long)h.bytes);
   char* out = static_cast<char*>(dst);
@@ -866,6 +987,7 @@ static gts_status blob_write(const gts_bins* b, const gts_blob_info* info, void*
   std::memcpy(out, &h, sizeof(h));
   std::memcpy(out + h.off_bias, b->tab->bias.data(), 8 * b->tab->bias.size());
   if (h.layout == GTS_LAYOUT_NODAL) {
+    const NodalPlan& np = pc->np;
     if (h.dtype == GTS_F32) write_gauss<float>(out + h.off_gauss);
     else write_gauss<double>(out + h.off_gauss);
     std::memcpy(out + h.off_units, np.chunks.data(), sizeof(ChunkRec) * np.chunks.size());
@@ -877,11 +999,11 @@ static gts_status blob_write(const gts_bins* b, const gts_blob_info* info, void*
       wi[c + 1] = wi[c] + np.work_inter[c];
     }
     std::memcpy(out + h.off_slotmap, np.slotmap.data(), 4 * np.slotmap.size());
-    if (h.dtype == GTS_F32) write_regions<float>(np, h.max_slots, out);
-    else write_regions<double>(np, h.max_slots, out);
+    if (h.dtype == GTS_F32) write_regions<float>(*b->tab, np, h.max_slots, h.n_tables, out);
+    else write_regions<double>(*b->tab, np, h.max_slots, h.n_tables, out);
   } else {
-    if (h.dtype == GTS_F32) write_bins<float>(*b, bp, h, out);
-    else write_bins<double>(*b, bp, h, out);
+    if (h.dtype == GTS_F32) write_bins<float>(*b, pc->bp, h, out);
+    else write_bins<double>(*b, pc->bp, h, out);
   }
   return GTS_OK;
 }
@@ -959,7 +1081,18 @@ void gts_bins_free(gts_bins* b) { delete b; }
 gts_status gts_blob_plan(const gts_bins* bins, gts_dtype dtype, gts_layout layout, int32_t max_slots,
                          gts_blob_info* info) {
   try {
-    return gts::blob_plan(bins, (int32_t)dtype, (int32_t)layout, max_slots, info, nullptr, nullptr, nullptr);
+    return gts::blob_plan_cached(bins, (int32_t)dtype, (int32_t)layout, max_slots, 0, info);
+  } catch (const std::bad_alloc&) {
+    return gts::fail(GTS_ERR_OUT_OF_MEMORY, "out of host memory");
+  }
+}
+
+gts_status gts_blob_plan_for(const gts_bins* bins, gts_dtype dtype, gts_layout layout, int32_t max_slots,
+                             gts_blob_use uses, gts_blob_info* info) {
+  if ((int32_t)uses < GTS_USE_SHAP || (int32_t)uses > GTS_USE_BOTH)
+    return gts::fail(GTS_ERR_INVALID_ARGUMENT, "bad blob uses %d", (int)uses);
+  try {
+    return gts::blob_plan_cached(bins, (int32_t)dtype, (int32_t)layout, max_slots, (int32_t)uses, info);
   } catch (const std::bad_alloc&) {
     return gts::fail(GTS_ERR_OUT_OF_MEMORY, "out of host memory");
   }

@@ -110,6 +110,20 @@ bool uses_mirror(const gts_blob_info* info) {
          info->max_slots < info->n_features;
 }
 
+// ------------------------------------------------- X validation (reading G17)
+
+// first[0] = smallest linear (row * M + feature) index of a non-finite X entry
+template <typename T>
+__global__ void nonfinite_kernel(const T* __restrict__ X, int64_t n_rows, int M, int64_t rs, int64_t cs,
+                                 unsigned long long* first) {
+  const int64_t total = n_rows * M;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / M, f = i - r * M;
+    const T v = X[r * rs + f * cs];
+    if (!isfinite(v)) atomicMin(first, (unsigned long long)i);
+  }
+}
+
 // ------------------------------------------------------------- launchers
 
 constexpr int64_t kBiasOffset = 256;  // align256(sizeof(BlobHeader)), host.cpp blob_plan
@@ -220,18 +234,49 @@ gts_status launch_nodal_s(const gts_blob_info* info, const char* d_blob, const v
   switch (info->max_slots) {
     case 8: return launch_nodal<T, kInter, 8>(info, d_blob, d_X, n_rows, rs, cs, out, st, out_phi);
     case 16: return launch_nodal<T, kInter, 16>(info, d_blob, d_X, n_rows, rs, cs, out, st, out_phi);
-    case 32:
-      if constexpr (kInter) break;
-      else return launch_nodal<T, kInter, 32>(info, d_blob, d_X, n_rows, rs, cs, out, st);
+    case 32: return launch_nodal<T, kInter, 32>(info, d_blob, d_X, n_rows, rs, cs, out, st, out_phi);
     case 64:
       if constexpr (kInter) break;
       else return launch_nodal<T, kInter, 64>(info, d_blob, d_X, n_rows, rs, cs, out, st);
     default: break;
   }
-  return fail(GTS_ERR_INVALID_ARGUMENT,
-              kInter ? "interaction kernel needs a NODAL blob with max_slots 8 or 16 (got %d)"
-                     : "unsupported max_slots %d",
-              info->max_slots);
+  return fail(GTS_ERR_INVALID_ARGUMENT, "unsupported max_slots %d", info->max_slots);
+}
+
+// Shared memory of the NODAL launch for this blob (0 = no such kernel).
+template <typename T, bool kInter>
+size_t nodal_smem_for(const gts_blob_info* info) {
+  switch (info->max_slots) {
+    case 8: return nodal_smem_bytes<T, kInter, 8>(info);
+    case 16: return nodal_smem_bytes<T, kInter, 16>(info);
+    case 32: return nodal_smem_bytes<T, kInter, 32>(info);
+    case 64: return kInter ? 0 : nodal_smem_bytes<T, kInter, 64>(info);
+    default: return 0;
+  }
+}
+
+// NODAL blob / kernel compatibility, checked before anything is launched
+// (the init fills overwrite the caller's outputs).
+gts_status check_nodal(const gts_blob_info* info, bool inter) {
+  if (info->layout != GTS_LAYOUT_NODAL || info->n_units == 0) return GTS_OK;
+  const int S = info->max_slots;
+  if (inter) {
+    if (!(info->uses & GTS_USE_INTERACTIONS) || info->n_tables != 3 || (S != 8 && S != 16 && S != 32))
+      return fail(GTS_ERR_INVALID_ARGUMENT,
+                  "the interaction kernel needs a NODAL blob planned for interactions (uses %d, max_slots %d): "
+                  "use gts_blob_plan_for(..., GTS_USE_INTERACTIONS, ...)", info->uses, S);
+  } else {
+    if (!(info->uses & GTS_USE_SHAP) || info->n_tables != nodal_tables(S) ||
+        (S != 8 && S != 16 && S != 32 && S != 64))
+      return fail(GTS_ERR_INVALID_ARGUMENT,
+                  "the SHAP kernel needs a NODAL blob planned for SHAP (uses %d, max_slots %d, %d tables)", info->uses,
+                  S, info->n_tables);
+  }
+  const size_t smem = info->dtype == GTS_F32 ? (inter ? nodal_smem_for<float, true>(info) : nodal_smem_for<float, false>(info))
+                                             : (inter ? nodal_smem_for<double, true>(info) : nodal_smem_for<double, false>(info));
+  if (smem == 0 || smem > 227 * 1024)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "chunk staging needs %zu bytes of shared memory", smem);
+  return GTS_OK;
 }
 
 template <typename T, bool kInter>
@@ -285,6 +330,8 @@ gts_status run(const gts_blob_info* info, const void* d_blob, const void* d_X, i
                void* d_out, void* stream) {
   gts_status s = check_call(info, d_blob, d_X, n_rows, rs, cs, d_out);
   if (s != GTS_OK || n_rows == 0) return s;
+  s = check_nodal(info, kInter);
+  if (s != GTS_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const char* blob = static_cast<const char*>(d_blob);
   const bool f32 = info->dtype == GTS_F32;
@@ -307,6 +354,8 @@ gts_status run_fused(const gts_blob_info* info, const void* d_blob, const void* 
   gts_status s = check_call(info, d_blob, d_X, n_rows, rs, cs, d_phi_ij);
   if (s != GTS_OK || n_rows == 0) return s;
   s = check_call(info, d_blob, d_X, n_rows, rs, cs, d_phi);
+  if (s != GTS_OK) return s;
+  s = check_nodal(info, true);
   if (s != GTS_OK) return s;
   if (info->layout != GTS_LAYOUT_NODAL) {
     s = run<true>(info, d_blob, d_X, n_rows, rs, cs, d_phi_ij, stream);
@@ -355,6 +404,39 @@ gts_status gts_shap_and_interactions(const gts_blob_info* info, const void* d_bl
                                      int64_t row_stride, int64_t col_stride, void* d_phi, void* d_phi_ij,
                                      void* stream) {
   return gts::run_fused(info, d_blob, d_X, n_rows, row_stride, col_stride, d_phi, d_phi_ij, stream);
+}
+
+gts_status gts_validate_x(gts_dtype dtype, const void* d_X, int64_t n_rows, int32_t n_features, int64_t row_stride,
+                          int64_t col_stride, void* stream) {
+  if (dtype != GTS_F32 && dtype != GTS_F64) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "bad dtype");
+  if (n_rows < 0 || n_features < 1) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (n_rows == 0) return GTS_OK;
+  if (!d_X) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "NULL X");
+  const bool row_major = col_stride == 1 && row_stride >= n_features;
+  const bool feature_major = row_stride == 1 && col_stride >= n_rows;
+  if (!row_major && !feature_major) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "bad X strides");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* d_first = nullptr;
+  if (cudaMallocAsync(&d_first, sizeof(unsigned long long), st) != cudaSuccess)
+    return gts::fail(GTS_ERR_CUDA, "cudaMallocAsync failed");
+  cudaMemsetAsync(d_first, 0xff, sizeof(unsigned long long), st);
+  const int64_t total = n_rows * n_features;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)gts::num_sms() * 8);
+  if (dtype == GTS_F32)
+    gts::nonfinite_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(d_X), n_rows, n_features,
+                                                         row_stride, col_stride, d_first);
+  else
+    gts::nonfinite_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(d_X), n_rows, n_features,
+                                                          row_stride, col_stride, d_first);
+  unsigned long long first = ~0ull;
+  cudaMemcpyAsync(&first, d_first, sizeof(first), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_first, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return gts::fail(GTS_ERR_CUDA, "gts_validate_x: %s", cudaGetErrorString(e));
+  if (first != ~0ull)
+    return gts::fail(GTS_ERR_NONFINITE, "X[%llu][%llu] is not finite (reading G17: X must be finite)",
+                     first / (unsigned long long)n_features, first % (unsigned long long)n_features);
+  return GTS_OK;
 }
 
 int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions) {

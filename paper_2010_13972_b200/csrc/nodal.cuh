@@ -892,7 +892,10 @@ struct Cfg {
                            : ((sizeof(T) == 4 && !kInter && S <= 16) ? 2
                               : ((sizeof(T) == 4 && !kInter) ? GTS_SHAP_R_WIDE : 1));
   static constexpr int tile_bytes = (int)sizeof(T) * tile_words_per_warp<T, S, R, kInter>();
-  static constexpr int W = tile_bytes * 8 <= 74 * 1024 ? 8 : (tile_bytes * 4 <= 80 * 1024 ? 4 : 2);
+  static constexpr int W = tile_bytes * 8 <= 74 * 1024   ? 8
+                           : tile_bytes * 4 <= 80 * 1024  ? 4
+                           : tile_bytes * 2 <= 160 * 1024 ? 2
+                                                          : 1;  // 32-slot interaction tiles (528 pair cells per row)
   static constexpr int kMinBlocks = 2;
 };
 
@@ -1119,7 +1122,7 @@ __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a)
       const T* tab = reinterpret_cast<const T*>(sP + c.n_paths);
       for (int p = 0; p < c.n_paths;) {
         const int4 ph = sP[p];
-        run_dispatch<T, R, kInter, nodal_tables(S)>(ph, sE, tab, sT, xb, ab);
+        run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S)>(ph, sE, tab, sT, xb, ab);
         p += ph.x >> 16;
       }
       dirty = true;

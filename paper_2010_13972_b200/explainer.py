@@ -27,7 +27,10 @@ class Blob:
 
     @classmethod
     def from_bins(cls, bins: gts.Bins, dtype: int, layout, max_slots: int, device) -> "Blob":
-        info = gts.gts_blob_plan(bins, dtype, layout, max_slots)
+        return cls.from_info(bins, gts.gts_blob_plan(bins, dtype, layout, max_slots), device)
+
+    @classmethod
+    def from_info(cls, bins: gts.Bins, info: gts.gts_blob_info, device) -> "Blob":
         host = torch.empty(info.bytes, dtype=torch.uint8, pin_memory=torch.cuda.is_available())
         gts.gts_blob_write(bins, info, host.numpy())
         dev = host.to(device, non_blocking=True) if device is not None else host
@@ -60,23 +63,91 @@ class TreeShapExplainer:
     """
 
     def __init__(self, model, dtype: str = "f32", pack: str = "bfd", layout: str = "nodal",
-                 device=None, max_slots: int = 0, interactions: bool = True, build_blobs: bool = True):
+                 device=None, max_slots: int = 0, interactions: bool = True, build_blobs: bool = True,
+                 inter_max_slots: int = 0, validate: bool = False):
+        """interactions: build the interaction blob now (True) or on the first
+        interaction call (False); it is never a reason to fail.  build_blobs=False
+        defers both blobs (multi-GPU ranks that receive them by broadcast).
+        validate: check every X for NaN / inf first (gts_validate_x, reading
+        G17; costs a pass over X and a stream synchronisation)."""
+        self.validate = bool(validate)
         self.dtype_code, self.torch_dtype, self.np_dtype = _DT[dtype]
         self.layout = gts.LAYOUTS[layout] if isinstance(layout, str) else int(layout)
         self.device = torch.device(device) if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None)
         self.n_features = int(model.n_features)
         self.n_groups = int(model.n_groups)
+        self.max_slots = int(max_slots)
+        self.inter_max_slots = int(inter_max_slots)
         self.paths = gts.gts_extract_paths(model)
         self.bins = gts.gts_binpack(self.paths, 32, pack)
-        self.blob = self.blob_int = None
+        self._blob = self._blob_int = None
         if build_blobs:
-            self.blob = Blob.from_bins(self.bins, self.dtype_code, self.layout, max_slots, self.device)
+            self._blob = self._make_blob(False)
             if interactions:
-                if self.layout == gts.GTS_LAYOUT_NODAL and self.blob.info.max_slots > 16:
-                    self.blob_int = Blob.from_bins(self.bins, self.dtype_code, self.layout, 16, self.device)
-                else:
-                    self.blob_int = self.blob
+                _ = self.blob_int
+
+    def _make_blob(self, for_interactions: bool) -> Blob:
+        if self.layout == gts.GTS_LAYOUT_NODAL and for_interactions:
+            info = gts.gts_blob_plan_for(self.bins, self.dtype_code, self.layout, self.inter_max_slots,
+                                         "interactions")
+            return Blob.from_info(self.bins, info, self.device)
+        return Blob.from_bins(self.bins, self.dtype_code, self.layout, self.max_slots, self.device)
+
+    @property
+    def blob(self) -> Blob:
+        """The blob gts_shap reads (built on first use when deferred)."""
+        if self._blob is None:
+            self._blob = self._make_blob(False)
+        return self._blob
+
+    @blob.setter
+    def blob(self, b: Blob):
+        self._blob = b
+
+    @property
+    def blob_int(self) -> Blob:
+        """The blob the interaction calls read: the SHAP blob itself when it
+        carries the interaction tables (NODAL with <= 16 slots, WARP_BINS),
+        else a blob planned for interactions (16 slots, or 32 when a merged
+        path has more than 16 features)."""
+        if self._blob_int is None:
+            b = self._blob
+            if b is not None and b.info is not None and (self.layout == gts.GTS_LAYOUT_WARP_BINS or
+                                                         (b.info.uses & gts.GTS_USE_INTERACTIONS)):
+                self._blob_int = b
+            else:
+                self._blob_int = self._make_blob(True)
+        return self._blob_int
+
+    @blob_int.setter
+    def blob_int(self, b: Blob):
+        self._blob_int = b
+
+    # ------------------------------------------------------------ validation
+    def _check_x(self, X) -> None:
+        if not isinstance(X, torch.Tensor):
+            raise TypeError("X must be a torch tensor on the explainer's device (use shap() for host arrays)")
+        if X.device != self.device:
+            raise ValueError(f"X is on {X.device}, the explainer on {self.device}")
+        if X.dtype != self.torch_dtype:
+            raise ValueError(f"X has dtype {X.dtype}, the explainer computes in {self.torch_dtype}")
+        if X.dim() != 2 or X.shape[1] < self.n_features:
+            raise ValueError(f"X must be [n_rows][>= {self.n_features}] (got shape {tuple(X.shape)})")
+        if self.validate:
+            self.validate_x(X)
+
+    def validate_x(self, X: torch.Tensor, stream=None) -> None:
+        """Raise gts.GtsError (GTS_ERR_NONFINITE) if X holds NaN or +-inf (reading G17)."""
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rs, cs = self._strides(X)
+        gts.gts_validate_x(self.dtype_code, X.data_ptr(), X.shape[0], self.n_features, rs, cs, st.cuda_stream)
+
+    def _check_out(self, out, shape) -> None:
+        if not isinstance(out, torch.Tensor) or out.device != self.device or out.dtype != self.torch_dtype:
+            raise ValueError(f"out must be a {self.torch_dtype} tensor on {self.device}")
+        if tuple(out.shape) != tuple(shape) or not out.is_contiguous():
+            raise ValueError(f"out must be contiguous with shape {tuple(shape)} (got {tuple(out.shape)})")
 
     # ------------------------------------------------------------------ device
     def _device_x(self, X):
@@ -104,9 +175,12 @@ class TreeShapExplainer:
 
     def shap_device(self, X: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """phi [n_rows][G][M+1] on the device (X already on the device, row- or feature-major)."""
+        self._check_x(X)
         n = X.shape[0]
+        shape = (n, self.n_groups, self.n_features + 1)
         if out is None:
-            out = torch.empty((n, self.n_groups, self.n_features + 1), dtype=self.torch_dtype, device=self.device)
+            out = torch.empty(shape, dtype=self.torch_dtype, device=self.device)
+        self._check_out(out, shape)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         rs, cs = self._strides(X)
         gts.gts_shap_strided(self.blob.info, self.blob.ptr, X.data_ptr(), n, rs, cs, out.data_ptr(), st.cuda_stream)
@@ -114,10 +188,12 @@ class TreeShapExplainer:
 
     def interactions_device(self, X: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """phi_ij [n_rows][G][M+1][M+1] on the device."""
+        self._check_x(X)
         n = X.shape[0]
         M1 = self.n_features + 1
         if out is None:
             out = torch.empty((n, self.n_groups, M1, M1), dtype=self.torch_dtype, device=self.device)
+        self._check_out(out, (n, self.n_groups, M1, M1))
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         rs, cs = self._strides(X)
         gts.gts_shap_interactions_strided(self.blob_int.info, self.blob_int.ptr, X.data_ptr(), n, rs, cs,
@@ -128,12 +204,15 @@ class TreeShapExplainer:
                                      out_phi_ij: torch.Tensor | None = None, stream=None):
         """(phi, phi_ij) of the same rows from one pass (gts_shap_and_interactions):
         the interaction kernel also writes the SHAP values, no SHAP kernel runs."""
+        self._check_x(X)
         n = X.shape[0]
         M1 = self.n_features + 1
         if out_phi is None:
             out_phi = torch.empty((n, self.n_groups, M1), dtype=self.torch_dtype, device=self.device)
         if out_phi_ij is None:
             out_phi_ij = torch.empty((n, self.n_groups, M1, M1), dtype=self.torch_dtype, device=self.device)
+        self._check_out(out_phi, (n, self.n_groups, M1))
+        self._check_out(out_phi_ij, (n, self.n_groups, M1, M1))
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         rs, cs = self._strides(X)
         gts.gts_shap_and_interactions(self.blob_int.info, self.blob_int.ptr, X.data_ptr(), n, rs, cs,
@@ -141,7 +220,8 @@ class TreeShapExplainer:
         return out_phi, out_phi_ij
 
     def explain_host_pipelined(self, X_host: torch.Tensor, phi_host: torch.Tensor | None = None,
-                               phi_ij_host: torch.Tensor | None = None, chunk_rows: int = 1 << 17):
+                               phi_ij_host: torch.Tensor | None = None, chunk_rows: int = 1 << 17,
+                               device_budget_bytes: int = 8 << 30):
         """Host rows in, host outputs out, with the copies hidden behind the kernels.
 
         X_host [n][M] and the outputs (phi_host [n][G][M+1] and/or phi_ij_host
@@ -158,7 +238,10 @@ class TreeShapExplainer:
             raise ValueError("no output requested")
         if n == 0:
             return phi_host, phi_ij_host
-        cr = max(1, min(int(chunk_rows), n))
+        esz = torch.tensor([], dtype=self.torch_dtype).element_size()
+        row_bytes = esz * (M + (G * M1 if want_phi else 0) + (G * M1 * M1 if want_ij else 0))
+        # two device slots of cr rows each stay within device_budget_bytes
+        cr = max(1, min(int(chunk_rows), n, int(device_budget_bytes) // (2 * row_bytes)))
         dev = self.device
         main = torch.cuda.current_stream(dev)
         if not hasattr(self, "_pipe_streams"):

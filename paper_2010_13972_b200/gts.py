@@ -24,6 +24,8 @@ GTS_PACK_FFD, GTS_PACK_BFD, GTS_PACK_NF, GTS_PACK_NONE = 0, 1, 2, 3
 PACK_ALGOS = {"ffd": 0, "bfd": 1, "nf": 2, "none": 3}
 GTS_F32, GTS_F64 = 0, 1
 GTS_LAYOUT_NODAL, GTS_LAYOUT_WARP_BINS = 0, 1
+GTS_USE_SHAP, GTS_USE_INTERACTIONS, GTS_USE_BOTH = 1, 2, 3
+USES = {"shap": 1, "interactions": 2, "both": 3}
 LAYOUTS = {"nodal": 0, "warp_bins": 1}
 
 _i64, _i32, _u32, _dbl, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_double, ctypes.c_void_p
@@ -59,7 +61,7 @@ class gts_blob_info(ctypes.Structure):
                 ("shap_flops_per_row", _dbl), ("inter_flops_per_row", _dbl),
                 ("paper_shap_flops_per_row", _dbl), ("paper_inter_flops_per_row", _dbl),
                 ("max_chunk_bytes", _i64), ("max_chunk_elems", _i64), ("max_chunk_paths", _i64),
-                ("reserved", _i64 * 5)]
+                ("uses", _i32), ("n_tables", _i32), ("reserved", _i64 * 4)]
 
     def to_bytes(self) -> bytes:
         return ctypes.string_at(ctypes.addressof(self), ctypes.sizeof(self))
@@ -76,9 +78,9 @@ class gts_blob_info(ctypes.Structure):
 
 # The symbols the header declares (checked by tests/test_abi.py).
 EXPORTS = ["gts_extract_paths", "gts_paths_view_get", "gts_paths_free", "gts_binpack", "gts_bins_view_get",
-           "gts_bins_free", "gts_blob_plan", "gts_blob_write", "gts_shap", "gts_shap_interactions",
+           "gts_bins_free", "gts_blob_plan", "gts_blob_plan_for", "gts_blob_write", "gts_shap", "gts_shap_interactions",
            "gts_shap_strided", "gts_shap_interactions_strided", "gts_shap_and_interactions",
-           "gts_launches_per_call", "gts_last_error", "gts_status_string", "gts_abi_version"]
+           "gts_validate_x", "gts_launches_per_call", "gts_last_error", "gts_status_string", "gts_abi_version"]
 
 _lib = None
 
@@ -102,6 +104,7 @@ def load(path: str = LIB_PATH):
     lib.gts_bins_free.argtypes = [_vp]
     lib.gts_bins_free.restype = None
     lib.gts_blob_plan.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _i32, P(gts_blob_info)]
+    lib.gts_blob_plan_for.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _i32, ctypes.c_int, P(gts_blob_info)]
     lib.gts_blob_write.argtypes = [_vp, P(gts_blob_info), _vp, ctypes.c_size_t]
     for name in ("gts_shap", "gts_shap_interactions"):
         fn = getattr(lib, name)
@@ -112,6 +115,8 @@ def load(path: str = LIB_PATH):
         fn.restype = ctypes.c_int
     lib.gts_shap_and_interactions.argtypes = [P(gts_blob_info), _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]
     lib.gts_shap_and_interactions.restype = ctypes.c_int
+    lib.gts_validate_x.argtypes = [ctypes.c_int, _vp, _i64, _i32, _i64, _i64, _vp]
+    lib.gts_validate_x.restype = ctypes.c_int
     lib.gts_launches_per_call.argtypes = [P(gts_blob_info), _i32]
     lib.gts_launches_per_call.restype = _i32
     lib.gts_last_error.argtypes = []
@@ -121,6 +126,7 @@ def load(path: str = LIB_PATH):
     lib.gts_abi_version.argtypes = []
     lib.gts_abi_version.restype = _i32
     for name in ("gts_extract_paths", "gts_paths_view_get", "gts_binpack", "gts_bins_view_get", "gts_blob_plan",
+                 "gts_blob_plan_for",
                  "gts_blob_write", "gts_shap", "gts_shap_interactions"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -222,6 +228,16 @@ def gts_blob_plan(bins: Bins, dtype=GTS_F32, layout=GTS_LAYOUT_NODAL, max_slots:
     return info
 
 
+def gts_blob_plan_for(bins: Bins, dtype=GTS_F32, layout=GTS_LAYOUT_NODAL, max_slots: int = 0,
+                      uses="both") -> gts_blob_info:
+    """gts_blob_plan for an explicit use ("shap", "interactions", "both" or a GTS_USE_* value)."""
+    info = gts_blob_info()
+    lay = LAYOUTS[layout] if isinstance(layout, str) else int(layout)
+    u = USES[uses] if isinstance(uses, str) else int(uses)
+    _check(load().gts_blob_plan_for(bins.handle, int(dtype), lay, int(max_slots), u, ctypes.byref(info)))
+    return info
+
+
 def gts_blob_write(bins: Bins, info: gts_blob_info, dst=None) -> np.ndarray:
     """Serialise the blob into a (new or given) uint8 host array."""
     if dst is None:
@@ -263,6 +279,13 @@ def gts_shap_and_interactions(info: gts_blob_info, d_blob: int, d_x: int, n_rows
     """(3)+(4) in one pass: SHAP values and interaction values of the same rows."""
     _check(load().gts_shap_and_interactions(ctypes.byref(info), d_blob, d_x, int(n_rows), int(row_stride),
                                             int(col_stride), d_phi, d_phi_ij, stream or None))
+
+
+def gts_validate_x(dtype, d_x: int, n_rows: int, n_features: int, row_stride: int, col_stride: int,
+                   stream: int = 0):
+    """Reading G17: raise GtsError(GTS_ERR_NONFINITE) if X holds NaN / inf (synchronises the stream)."""
+    _check(load().gts_validate_x(int(dtype), d_x, int(n_rows), int(n_features), int(row_stride), int(col_stride),
+                                 stream or None))
 
 
 def gts_launches_per_call(info: gts_blob_info, interactions) -> int:

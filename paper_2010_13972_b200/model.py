@@ -29,6 +29,7 @@ class TreeModel:
     n_features: int
     n_groups: int
     base_score: float = 0.0
+    cover_adjust: float = 0.0  # largest relative change made by covers="conserve" (0 = none)
 
     @property
     def n_trees(self) -> int:
@@ -61,8 +62,21 @@ def _feature_index(name, feature_map, where):
     return int(m.group(1))
 
 
+def _conserve_covers(left, right, cover):
+    """Internal covers := sum of their children's, bottom-up in fp64 (root
+    first ordering: every child index is larger than its parent's).  Returns
+    the largest relative change."""
+    worst = 0.0
+    for j in range(len(left) - 1, -1, -1):
+        if left[j] >= 0:
+            c = cover[left[j]] + cover[right[j]]
+            worst = max(worst, abs(c - cover[j]) / c)
+            cover[j] = c
+    return worst
+
+
 def from_xgboost_dump(doc, num_class: int = 1, feature_map=None, n_features: int | None = None,
-                      base_score: float = 0.0) -> TreeModel:
+                      base_score: float = 0.0, covers: str = "conserve", cover_rtol: float = 1e-4) -> TreeModel:
     """Parse XGBoost `Booster.dump_model(..., dump_format="json")` output.
 
     doc: the JSON text, or the already-parsed list of tree objects.  Each node
@@ -72,7 +86,21 @@ def from_xgboost_dump(doc, num_class: int = 1, feature_map=None, n_features: int
     SPEC.md:63).  feature_map maps split names to indices when they are not
     "f<k>".  n_features defaults to 1 + the largest split index.  A "missing"
     branch that is neither "yes" nor "no" is rejected (X must be finite, G17).
+
+    covers: XGBoost stores each node's hessian sum as float32 and the dump
+    prints it at limited precision, so a parent's printed cover differs from
+    the sum of its children's by up to ~1e-6 relative -- at or beyond the
+    library's 1e-6 conservation check.  "conserve" (default)
+    rebuilds every internal cover as the sum of its children's, bottom-up in
+    fp64 from the printed leaf covers (the relative change, ~1e-7, is kept in
+    ``cover_adjust``; z = r_child / r_parent then changes by as much, far below
+    fp32 kernel rounding); "as_is" passes the printed covers through, and the
+    library rejects the model if they do not conserve.  A printed cover that
+    is off by more than cover_rtol (relative) is a broken dump, not rounding:
+    DumpError.
     """
+    if covers not in ("conserve", "as_is"):
+        raise DumpError("covers must be 'conserve' or 'as_is'")
     trees = json.loads(doc) if isinstance(doc, (str, bytes)) else doc
     if not isinstance(trees, list):
         raise DumpError("dump must be a JSON array of tree objects")
@@ -80,6 +108,7 @@ def from_xgboost_dump(doc, num_class: int = 1, feature_map=None, n_features: int
         raise DumpError("num_class must be >= 1")
     L, R, F, TH, C, V, off = [], [], [], [], [], [], [0]
     max_f = -1
+    adjust = 0.0
     for t, root in enumerate(trees):
         nodes = {}
         stack = [root]
@@ -107,6 +136,7 @@ def from_xgboost_dump(doc, num_class: int = 1, feature_map=None, n_features: int
             if "leaf" not in nd:
                 stack.append(int(nd["no"]))
                 stack.append(int(nd["yes"]))
+        c0 = len(C)
         for nid in order:
             nd = nodes[nid]
             where = f"tree {t} node {nid}"
@@ -126,9 +156,17 @@ def from_xgboost_dump(doc, num_class: int = 1, feature_map=None, n_features: int
             max_f = max(max_f, f)
             L.append(local[yes]); R.append(local[no]); F.append(f)
             TH.append(float(nd["split_condition"])); V.append(0.0)
+        if covers == "conserve":
+            lt, rt, ct = L[c0:], R[c0:], C[c0:]
+            worst = _conserve_covers(lt, rt, ct)
+            if worst > cover_rtol:
+                raise DumpError(f"tree {t}: cover(parent) differs from cover(left) + cover(right) by "
+                                f"{worst:.3g} relative (> cover_rtol {cover_rtol:g})")
+            adjust = max(adjust, worst)
+            C[c0:] = ct
         off.append(off[-1] + len(order))
     m = (max_f + 1) if n_features is None else int(n_features)
     return TreeModel(np.array(off, np.int64), np.array(L, np.int32), np.array(R, np.int32),
                      np.array(F, np.int32), np.array(TH, np.float32), np.array(C, np.float64),
                      np.array(V, np.float64), np.array([t % num_class for t in range(len(trees))], np.int32),
-                     max(m, 1), int(num_class), float(base_score))
+                     max(m, 1), int(num_class), float(base_score), float(adjust))

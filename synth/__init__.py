@@ -44,7 +44,7 @@ def _load():
         build()
         lib = ctypes.CDLL(_SO)
         i64, i32, dbl, u64, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_uint64, ctypes.c_void_p
-        lib.synth_grow_ensemble.argtypes = [i64, i32, i32, i32, dbl, dbl, dbl, dbl, u64, i64,
+        lib.synth_grow_ensemble.argtypes = [i64, i32, i32, i32, dbl, dbl, dbl, dbl, u64, dbl, i64,
                                             vp, vp, vp, vp, vp, vp, vp]
         lib.synth_grow_ensemble.restype = ctypes.c_int
         lib.synth_fill_x_f32.argtypes = [u64, i64, i64, i32, vp]
@@ -133,9 +133,12 @@ def ensemble_from_trees(trees, n_features: int, n_groups: int = 1, groups=None,
 
 def make_ensemble(n_trees: int, n_features: int, max_depth: int, leaves_per_tree: float,
                   n_groups: int = 1, zipf_s: float = 1.0, beta: float = 0.0, seed: int = 0,
-                  root_cover: float = float(1 << 20), base_score: float = 0.0) -> Ensemble:
+                  root_cover: float = float(1 << 20), base_score: float = 0.0,
+                  cover_skew: float = 0.0) -> Ensemble:
     """Random-split ensemble (recipe: synth/_synth.c header).  Tree t belongs to
-    group t mod n_groups (XGBoost round-robin)."""
+    group t mod n_groups (XGBoost round-robin).  cover_skew > 0
+    draws skewed cover splits (zero fractions down to cover_skew); pair it with
+    a large root_cover (e.g. 2**50) so deep nodes keep integer covers >= 2."""
     lib = _load()
     lf = int(np.floor(leaves_per_tree))
     frac = float(leaves_per_tree - lf)
@@ -148,7 +151,7 @@ def make_ensemble(n_trees: int, n_features: int, max_depth: int, leaves_per_tree
     cov = np.empty(shape, np.float64); val = np.empty(shape, np.float64)
     nn = np.zeros(T, np.int64)
     rc = lib.synth_grow_ensemble(T, n_features, max_depth, lf, frac, zipf_s, beta, root_cover,
-                                 ctypes.c_uint64(seed & (2**64 - 1)), max_nodes,
+                                 ctypes.c_uint64(seed & (2**64 - 1)), float(cover_skew), max_nodes,
                                  left.ctypes.data, right.ctypes.data, feat.ctypes.data, thr.ctypes.data,
                                  cov.ctypes.data, val.ctypes.data, nn.ctypes.data)
     if rc != 0:
@@ -160,7 +163,7 @@ def make_ensemble(n_trees: int, n_features: int, max_depth: int, leaves_per_tree
     return Ensemble(off, left[keep], right[keep], feat[keep], thr[keep], cov[keep], val[keep], groups,
                     int(n_features), int(n_groups), float(base_score),
                     dict(n_trees=T, max_depth=max_depth, leaves_per_tree=leaves_per_tree,
-                         zipf_s=zipf_s, beta=beta, seed=seed))
+                         zipf_s=zipf_s, beta=beta, seed=seed, cover_skew=cover_skew))
 
 
 def make_x(seed: int, n_rows: int, n_features: int, row0: int = 0) -> np.ndarray:

@@ -14,7 +14,10 @@
  *     features (repeats along a path allowed -> exercises the merge);
  *   - threshold t = fp32 value strictly inside the node's feasible interval on
  *     that feature (x < t -> left, half-open bounds);
- *   - integer covers: c_left = clamp(round(r*C), 1, C-1), r ~ U(0.1, 0.9);
+ *   - integer covers: c_left = clamp(round(r*C), 1, C-1), r ~ U(0.1, 0.9); or,
+ *     with cover_skew = s in (0, 1), r log-uniform on [s, 1] and mirrored to
+ *     1 - r with probability 1/2, so per-edge cover ratios (zero fractions)
+ *     reach s and 1 - s (the skewed splits of real GBDT models);
  *   - stop at the tree's leaf target or when nothing is expandable;
  *   - leaf values fp32(N(0,1) * 0.01) (lr 0.01 scale).
  *   X[r][c] = U[0,1) fp32 from a counter-based hash of (seed, r, c): any row
@@ -65,6 +68,7 @@ typedef struct {
   double zipf_s, beta;
   double root_cover;
   uint64_t seed;
+  double cover_skew;    /* 0: r ~ U(0.1, 0.9); else log-uniform on [cover_skew, 1], mirrored */
 } synth_params;
 
 /*
@@ -146,7 +150,13 @@ static int64_t grow_tree(const synth_params* p, int64_t tree, int64_t max_nodes,
     if (!ok) continue; /* node stays a leaf, no longer expandable */
 
     double C = cover[node];
-    double rr = 0.1 + 0.8 * rng_u01(&rng);
+    double rr;
+    if (p->cover_skew > 0.0) {
+      rr = exp(log(p->cover_skew) * rng_u01(&rng));
+      if (rng_u01(&rng) < 0.5) rr = 1.0 - rr;
+    } else {
+      rr = 0.1 + 0.8 * rng_u01(&rng);
+    }
     double cl = floor(rr * C + 0.5);
     if (cl < 1.0) cl = 1.0;
     if (cl > C - 1.0) cl = C - 1.0;
@@ -176,10 +186,10 @@ static int64_t grow_tree(const synth_params* p, int64_t tree, int64_t max_nodes,
  */
 int synth_grow_ensemble(int64_t n_trees, int32_t n_features, int32_t max_depth,
                         int32_t leaves_floor, double leaves_frac, double zipf_s, double beta,
-                        double root_cover, uint64_t seed, int64_t max_nodes,
+                        double root_cover, uint64_t seed, double cover_skew, int64_t max_nodes,
                         int32_t* left, int32_t* right, int32_t* feature, float* threshold,
                         double* cover, double* leaf_value, int64_t* n_nodes) {
-  synth_params p = {n_features, max_depth, leaves_floor, leaves_frac, zipf_s, beta, root_cover, seed};
+  synth_params p = {n_features, max_depth, leaves_floor, leaves_frac, zipf_s, beta, root_cover, seed, cover_skew};
   if (max_depth >= 63) return -1;
   double* zipf_cdf = (double*)malloc(sizeof(double) * (size_t)n_features);
   double tot = 0.0;

@@ -44,7 +44,7 @@ def test_exports_every_declared_symbol():
 
 def test_version_and_status_strings():
     lib = gts.load()
-    assert lib.gts_abi_version() == 2
+    assert lib.gts_abi_version() == 3
     for code, name in gts.STATUS_NAMES.items():
         assert lib.gts_status_string(code).decode() == name
 
@@ -107,7 +107,7 @@ def test_blob_plan_and_call_argument_errors():
     assert _status(gts.gts_blob_plan, b, 0, 9, 0) == 1
     assert _status(gts.gts_blob_plan, b, 0, 0, 12) == 1
     info = gts.gts_blob_plan(b, gts.GTS_F32, "nodal")
-    assert info.magic == 0x47545342 and info.abi_version == 2 and info.bytes % 256 == 0
+    assert info.magic == 0x47545342 and info.abi_version == 3 and info.bytes % 256 == 0
     with pytest.raises(ValueError):
         gts.gts_blob_write(b, info, np.empty(16, np.uint8))
     # n_rows == 0 is a no-op; argument errors are caught before any CUDA call
@@ -125,6 +125,54 @@ def test_blob_plan_and_call_argument_errors():
     assert _status(gts.gts_shap_and_interactions, info, 16, 16, 4, 2, 1, 16, 0) == 1   # NULL phi_ij
     assert _status(gts.gts_shap_and_interactions, info, 16, 16, 4, 2, 1, 18, 16) == 1  # misaligned phi
     assert _status(gts.gts_shap_and_interactions, bad, 16, 16, 4, 2, 1, 16, 16) == 1
+
+
+def _chain(depth, n_features, seed=0):
+    """One chain tree on `depth` distinct features: a merged path with k = depth."""
+    rng = np.random.default_rng(seed)
+    feats = rng.permutation(n_features)[:depth]
+    nodes, cover, cur = [None], 2.0 ** 40, 0
+    for d in range(depth):
+        lc = float(np.floor(cover * 0.5))
+        li, ri = len(nodes), len(nodes) + 1
+        nodes += [None, {"leaf_value": 1.0, "cover": cover - lc}]
+        nodes[cur] = {"feature": int(feats[d]), "threshold": 0.5, "left": li, "right": ri, "cover": cover}
+        cur, cover = li, lc
+    nodes[cur] = {"leaf_value": -1.0, "cover": cover}
+    return nodes
+
+
+def test_blob_uses_and_slot_widths():
+    """gts_blob_plan_for: interaction blobs take 8/16/32 slots with 3 table rows;
+    a merged path of 17..31 features needs 32; the default
+    plan serves both kernels only up to 16 slots; kernels reject a blob planned
+    for the other one before any launch."""
+    d2 = gts.gts_binpack(gts.gts_extract_paths(synth.depth2()), 32, "bfd")
+    both = gts.gts_blob_plan(d2, gts.GTS_F32, "nodal")
+    assert (both.uses, both.n_tables, both.max_slots) == (gts.GTS_USE_BOTH, 3, 8)
+    long_ = gts.gts_binpack(gts.gts_extract_paths(synth.ensemble_from_trees([_chain(20, 40)], n_features=40)))
+    shap = gts.gts_blob_plan(long_, gts.GTS_F32, "nodal")
+    assert (shap.uses, shap.n_tables, shap.max_slots) == (gts.GTS_USE_SHAP, 2, 64)
+    inter = gts.gts_blob_plan_for(long_, gts.GTS_F64, "nodal", 0, "interactions")
+    assert (inter.uses, inter.n_tables, inter.max_slots) == (gts.GTS_USE_INTERACTIONS, 3, 32)
+    assert gts.gts_blob_write(long_, inter).nbytes == inter.bytes
+    assert _status(gts.gts_blob_plan_for, long_, gts.GTS_F32, "nodal", 0, "both") == 1   # BOTH above 16 slots
+    assert _status(gts.gts_blob_plan_for, long_, gts.GTS_F32, "nodal", 16, "interactions") == 1  # k = 20 > 16
+    assert _status(gts.gts_blob_plan_for, long_, gts.GTS_F32, "nodal", 64, "interactions") == 1
+    assert _status(gts.gts_blob_plan_for, long_, gts.GTS_F32, "nodal", 0, 7) == 1
+    wide = gts.gts_binpack(gts.gts_extract_paths(synth.make_ensemble(20, 100, 6, 30, seed=3)))
+    i16 = gts.gts_blob_plan_for(wide, gts.GTS_F32, "nodal", 0, "interactions")
+    assert (i16.max_slots, i16.n_tables) == (16, 3)
+    # wrong kernel for the blob: INVALID_ARGUMENT before anything is launched
+    assert _status(gts.gts_shap_interactions, shap, 256, 256, 4, 40, 256) == 1
+    assert _status(gts.gts_shap_and_interactions, shap, 256, 256, 4, 40, 1, 256, 512) == 1
+    assert _status(gts.gts_shap, inter, 256, 256, 4, 40, 256) == 1
+    # the write without a preceding plan re-plans from the info
+    again = gts.gts_blob_info.from_bytes(inter.to_bytes())
+    gts.gts_blob_plan(d2, gts.GTS_F32, "nodal")  # replaces the cached plan of d2 only
+    b1 = gts.gts_blob_write(long_, again)
+    gts.gts_blob_plan_for(long_, gts.GTS_F64, "nodal", 0, "interactions")
+    assert np.array_equal(b1, gts.gts_blob_write(long_, inter))
 
 
 def test_launch_count_and_info_roundtrip():

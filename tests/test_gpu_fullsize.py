@@ -50,15 +50,12 @@ def test_adult_large_full(gpu):
     xd = torch.from_numpy(x).cuda()
     phi = ex.shap_device(xd).cpu().numpy()
     _shap_checks("adult-large", ens, x, phi, _sample(w.rows, 40))
-    f = oracle.predict(ens, x[:2048].astype(np.float64))
-    assert np.all(np.abs(phi[:2048].sum(axis=2) - f) <= 1e-3 * np.maximum(1.0, np.abs(f)))
+    parity.check_local_accuracy(phi, oracle.predict(ens, x.astype(np.float64)), "f32", "adult-large")
     pij = ex.interactions_device(xd).cpu().numpy()
     rows = _sample(w.rows, 8, seed=1)
     parity.check(pij[rows], oracle.interactions(ens, x[rows].astype(np.float64)), "f32",
                  "adult-large sampled full-size interactions")
-    M = w.n_features
-    s = np.abs(phi[:, :, :M]).max(axis=2, keepdims=True)
-    assert np.all(np.abs(pij[:, :, :M, :M].sum(axis=3) - phi[:, :, :M]) <= 1e-3 * np.maximum(np.abs(phi[:, :, :M]), s))
+    parity.check_row_sums(pij, phi, "f32", "adult-large")
     assert _symmetric(pij)
 
 
@@ -71,8 +68,7 @@ def test_fashion_mnist_med_full_shap(gpu):
     ex = _explainer(ens, interactions=False)
     phi = ex.shap_device(torch.from_numpy(x).cuda()).cpu().numpy()
     _shap_checks("fashion_mnist-med", ens, x, phi, _sample(w.rows, 64))
-    f = oracle.predict(ens, x.astype(np.float64))
-    assert np.all(np.abs(phi.sum(axis=2) - f) <= 1e-3 * np.maximum(1.0, np.abs(f)))
+    parity.check_local_accuracy(phi, oracle.predict(ens, x.astype(np.float64)), "f32", "fashion_mnist-med")
 
 
 def test_fashion_mnist_med_interactions_streamed(gpu):
@@ -93,9 +89,7 @@ def test_fashion_mnist_med_interactions_streamed(gpu):
     for r0, r1, chunk in ex.iter_interactions(xd, chunk_rows=128):
         c = chunk.cpu().numpy()
         assert _symmetric(c), "symmetry"
-        ph = phi[r0:r1, :, :M]
-        s = np.abs(ph).max(axis=2, keepdims=True)
-        assert np.all(np.abs(c[:, :, :M, :M].sum(axis=3) - ph) <= 1e-3 * np.maximum(np.abs(ph), s)), "row sums"
+        parity.check_row_sums(c, phi[r0:r1], "f32", "fashion streamed")
         for r in range(r0, r1):
             if r in want:
                 got[r] = c[r - r0].astype(np.float64)
@@ -116,17 +110,15 @@ def test_covtype_large_full_shap(gpu):
     phi = ex.shap_device(torch.from_numpy(x).cuda()).cpu().numpy()
     assert np.all(np.isfinite(phi))
     _shap_checks("covtype-large", ens, x, phi, _sample(n, 16))
-    sub = _sample(n, 256, seed=3)
-    f = oracle.predict(ens, x[sub].astype(np.float64))
-    assert np.all(np.abs(phi[sub].sum(axis=2) - f) <= 1e-3 * np.maximum(1.0, np.abs(f)))
+    parity.check_local_accuracy(phi, oracle.predict(ens, x.astype(np.float64)), "f32", "covtype-large")
 
 
-def test_covtype_large_full_interactions_properties(gpu):
-    """covtype interactions with the full 8000-tree model: the oracle needs
-    ~8 core-minutes per row, so parity is by properties that hold at any size
-    (row sums = the SHAP kernel's values, which are oracle-checked above;
-    symmetry; the bias cell) plus element-wise parity of the same kernels on a
-    400-tree subset in test_gpu_parity.py."""
+def test_covtype_large_full_interactions(gpu):
+    """covtype interactions with the full 8000-tree model (Table 7 covtype-large
+    row), 2048 rows in one call: element-wise against O6 on 4
+    sampled rows (the oracle needs ~6 core-minutes per row), and on every row
+    the properties that hold at any size: row sums = the SHAP kernel's values,
+    symmetry, the bias cell and the zero bias row / column."""
     import torch
     w = WORKLOADS["covtype-large"]
     ens = w.ensemble()
@@ -137,9 +129,10 @@ def test_covtype_large_full_interactions_properties(gpu):
     phi = ex.shap_device(xd).cpu().numpy()
     pij = ex.interactions_device(xd).cpu().numpy()
     M = w.n_features
-    ph = phi[:, :, :M]
-    s = np.abs(ph).max(axis=2, keepdims=True)
-    assert np.all(np.abs(pij[:, :, :M, :M].sum(axis=3) - ph) <= 2e-3 * np.maximum(np.abs(ph), s))
+    parity.check_row_sums(pij, phi, "f32", "covtype-large")
     assert _symmetric(pij)
     np.testing.assert_allclose(pij[:, :, M, M], phi[:, :, M], rtol=1e-6)
     assert np.all(pij[:, :, :M, M] == 0) and np.all(pij[:, :, M, :M] == 0)
+    rows = np.array([0, 777, 1500, n - 1])
+    ref = parity.oracle_interactions_by_trees(ens, x[rows].astype(np.float64))
+    parity.check(pij[rows], ref, "f32", "covtype-large full-model interactions vs O6")

@@ -109,6 +109,44 @@ def test_configs_interactions(gpu, case, dtype, layout):
     parity.check(got, ref, dtype, f"{name} interactions")
 
 
+# ------------------------------------- skewed covers + x == t ties (wider input regime)
+
+SKEW = [
+    # (workload shape, trees kept, SHAP rows, interaction rows)
+    ("cal_housing-med", 100, 400, 48),
+    ("adult-large", 150, 64, 6),
+    ("covtype-large", 120, 32, 4),
+]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("case", SKEW, ids=[c[0] for c in SKEW])
+def test_skewed_covers_and_ties(gpu, case, dtype, layout):
+    """Real GBDT covers are skewed: per-edge zero fractions from 1e-4 to
+    1 - 1e-4 (synth cover_skew), where the fp32 nodal tables (rho = B/A,
+    C' = v w ((1-z)/A + 1/(1-t))) and the warp-bin o = 0 UNWIND division by z
+     are most exposed; plus 15 % of X entries exactly equal to a
+    split threshold of their feature (x == t goes right, reading G1)."""
+    import torch
+    name, trees, n, ni = case
+    w = WORKLOADS[name]
+    ens = synth.make_ensemble(trees, w.n_features, w.max_depth, w.leaves_per_tree, n_groups=w.n_groups,
+                              zipf_s=w.zipf_s, beta=w.beta, seed=w.seed + 1000, root_cover=2.0 ** 50,
+                              cover_skew=1e-4)
+    x = synth.inject_ties(w.x(n), ens, 0.15, seed=77)
+    ex = _explainer(ens, dtype, layout)
+    z = ex.paths.view()["zero_fraction"]
+    assert z.min() < 2e-4 and z[z < 1].max() > 1 - 2e-4  # the skewed regime is really exercised
+    x64 = x.astype(np.float64)
+    parity.check(_run(ex, x), oracle.treeshap(ens, x64), dtype, f"{name} skewed shap")
+    xd = torch.from_numpy(np.ascontiguousarray(x[:ni], dtype=ex.np_dtype)).cuda()
+    phi, phi_ij = ex.shap_and_interactions_device(xd)
+    torch.cuda.synchronize()
+    parity.check(phi.cpu().numpy(), oracle.treeshap(ens, x64[:ni]), dtype, f"{name} skewed fused shap")
+    parity.check(phi_ij.cpu().numpy(), oracle.interactions(ens, x64[:ni]), dtype, f"{name} skewed interactions")
+
+
 # ------------------------------------------------- fused SHAP + interactions
 
 FUSED = [c[:1] + (c[3], c[2]) for c in CASES if c[3] > 0] + [("fashion_mnist-med", 4, 120)]
@@ -248,8 +286,45 @@ def test_maximum_path_length(gpu, layout, dtype):
     ens = synth.ensemble_from_trees(trees, n_features=40)
     rng = np.random.default_rng(5)
     x = rng.uniform(0.25, 0.75, (64, 40)).astype(np.float32)
-    ex = _explainer(ens, dtype, layout, max_slots=0 if layout == "warp_bins" else 64, interactions=False)
+    ex = _explainer(ens, dtype, layout, max_slots=0 if layout == "warp_bins" else 64)
     parity.check(_run(ex, x), oracle.treeshap(ens, x.astype(np.float64)), dtype, "k=31 shap")
+    parity.check(_run(ex, x[:20], inter=True), oracle.interactions(ens, x[:20].astype(np.float64)), dtype,
+                 "k=31 interactions")
+
+
+def _long_path_model(n_features, seed=0):
+    """Chains with merged k = 31, 24 and 17 (the paper's bound is 31 features,
+    PAPER.md:213-217) plus a random depth-6 forest of short paths."""
+    trees = [_caterpillar(31, n_features, seed=seed + 1), _caterpillar(24, n_features, seed=seed + 2),
+             _caterpillar(17, n_features, seed=seed + 3)]
+    forest = synth.make_ensemble(12, n_features, 6, 30, zipf_s=0.5, seed=seed + 4)
+    trees += [_nodes_of(forest, t) for t in range(forest.n_trees)]
+    return synth.ensemble_from_trees(trees, n_features=n_features)
+
+
+@pytest.mark.parametrize("n_features", [31, 40], ids=["identity32", "slotmaps32"])
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_long_path_interactions(gpu, n_features, layout, dtype):
+    """Interaction values (and the fused call) on merged paths of 17..31
+    features: the default explainer builds a 32-slot interaction blob (NODAL),
+    identity slot map (M = 31) or per-chunk slot maps (M = 40)."""
+    import torch
+    ens = _long_path_model(n_features)
+    rng = np.random.default_rng(9)
+    x = rng.uniform(0.2, 0.8, (70, n_features)).astype(np.float32)
+    ex = _explainer(ens, dtype, layout)  # default arguments: must not fail
+    if layout == "nodal":
+        assert ex.blob_int.info.max_slots == 32 and ex.blob_int.info.n_tables == 3
+    x64 = x.astype(np.float64)
+    ref_ij = oracle.interactions(ens, x64)
+    parity.check(_run(ex, x, inter=True), ref_ij, dtype, f"k<=31 interactions M={n_features}")
+    parity.check(_run(ex, x), oracle.treeshap(ens, x64), dtype, f"k<=31 shap M={n_features}")
+    xd = torch.from_numpy(np.ascontiguousarray(x, dtype=ex.np_dtype)).cuda()
+    phi, phi_ij = ex.shap_and_interactions_device(xd[:33])
+    torch.cuda.synchronize()
+    parity.check(phi.cpu().numpy(), oracle.treeshap(ens, x64[:33]), dtype, "k<=31 fused shap")
+    parity.check(phi_ij.cpu().numpy(), ref_ij[:33], dtype, "k<=31 fused interactions")
 
 
 def test_path_too_long_rejected(gpu):
@@ -297,9 +372,11 @@ def test_packing_neutrality(gpu, pack):
 
 
 def test_local_accuracy_full_size(gpu):
-    """At the bench size (cal_housing-med, 2^20 rows, bench launch config):
-    sum(phi) + phi_0 = f(x) for every row (fp32: 1e-3 max(1,|f|)) and exact
-    parity on rows sampled across the whole range."""
+    """At the bench size (cal_housing-med, 2^20 rows, the launch configuration
+    bench.py times): the fused call (gts_shap_and_interactions) and the
+    separate calls, element-wise against O5 / O6 on rows sampled across the
+    whole range, and on every row additivity (sum phi + phi_0 = f(x)) and
+    Eq. 6 row sums at the normwise bar; fused and separate results agree."""
     import torch
     w = WORKLOADS["cal_housing-med"]
     ens = w.ensemble()
@@ -307,15 +384,26 @@ def test_local_accuracy_full_size(gpu):
     x = w.x(n, ens=ens)
     ex = _explainer(ens, "f32", "nodal")
     xd = torch.from_numpy(x).cuda()
-    phi = ex.shap_device(xd).cpu().numpy()
+    phi_f, phi_ij_f = ex.shap_and_interactions_device(xd)
+    phi_f, phi_ij_f = phi_f.cpu().numpy(), phi_ij_f.cpu().numpy()
     f = oracle.predict(ens, x.astype(np.float64))
-    assert np.all(np.abs(phi.sum(axis=2) - f) <= 1e-3 * np.maximum(1.0, np.abs(f)))
+    parity.check_local_accuracy(phi_f, f, "f32", "fused 2^20")
+    parity.check_row_sums(phi_ij_f, phi_f, "f32", "fused 2^20")
     rows = np.unique(np.r_[0, n - 1, np.random.default_rng(0).integers(0, n, 200)])
-    parity.check(phi[rows], oracle.treeshap(ens, x[rows].astype(np.float64)), "f32", "sampled full-size shap")
-    sub = rows[:32]
+    x64 = x[rows].astype(np.float64)
+    ref = oracle.treeshap(ens, x64)
+    parity.check(phi_f[rows], ref, "f32", "sampled full-size fused shap")
+    sub = rows[::6]
+    ref_ij = oracle.interactions(ens, x[sub].astype(np.float64))
+    parity.check(phi_ij_f[sub], ref_ij, "f32", "sampled full-size fused interactions")
+    del phi_ij_f
+    phi = ex.shap_device(xd).cpu().numpy()
+    parity.check_local_accuracy(phi, f, "f32", "shap 2^20")
+    parity.check(phi[rows], ref, "f32", "sampled full-size shap")
+    parity.check(phi, phi_f.astype(np.float64), "f32", "separate vs fused shap")
     phi_ij = ex.interactions_device(xd).cpu().numpy()
-    parity.check(phi_ij[sub], oracle.interactions(ens, x[sub].astype(np.float64)), "f32", "sampled interactions")
-    np.testing.assert_allclose(phi_ij[:, 0, :8, :8].sum(axis=2), phi[:, 0, :8], atol=2e-4)
+    parity.check(phi_ij[sub], ref_ij, "f32", "sampled full-size interactions")
+    parity.check_row_sums(phi_ij, phi, "f32", "separate 2^20")
 
 
 @pytest.mark.parametrize("layout", LAYOUTS)
@@ -388,3 +476,30 @@ def test_row_shards_and_replicated_blob(gpu):
     parity.check(cat, full.astype(np.float64), "f32", "shards vs single call")
     edge = sorted({c for b in cuts[1:-1] for c in (b - 1, b)})
     parity.check(cat[edge], oracle.treeshap(ens, x[edge].astype(np.float64)), "f32", "shard boundaries")
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_validate_nonfinite_x(gpu, dtype):
+    """Reading G17: gts_validate_x names the first non-finite entry (row-major
+    order) for row- and feature-major X; finite X passes; the explainer's
+    validate flag runs it before every call."""
+    import torch
+    from paper_2010_13972_b200 import gts
+    w = WORKLOADS["cal_housing-med"]
+    ens = w.ensemble().subset(range(10))
+    ex = _explainer(ens, dtype, interactions=False)
+    x = torch.from_numpy(np.ascontiguousarray(w.x(1000), dtype=ex.np_dtype)).cuda()
+    ex.validate_x(x)
+    ex.validate_x(x.t().contiguous().t())
+    for bad in (float("nan"), float("inf"), -float("inf")):
+        y = x.clone()
+        y[617, 5] = bad
+        y[901, 2] = bad
+        for z in (y, y.t().contiguous().t()):
+            with pytest.raises(gts.GtsError, match=r"X\[617\]\[5\]") as e:
+                ex.validate_x(z)
+            assert e.value.status == 4
+    ex.validate = True
+    with pytest.raises(gts.GtsError):
+        ex.shap_device(y)
+    ex.shap_device(x)

@@ -230,3 +230,15 @@ def test_pins_catch_a_dropped_half():
     doubled[0, 1] *= 2
     doubled[1, 0] *= 2
     assert not np.allclose(doubled[:2, :2], np.array(g["interactions"])[:2, :2])
+
+
+def test_oracle_interactions_split_over_trees():
+    """The tree-partitioned evaluation the full-size GPU tests use
+    (tests/parity.py: sum of O6 over tree subsets) equals one O6 call,
+    base_score included."""
+    from tests import parity
+    ens = synth.make_ensemble(9, 6, 5, 12, n_groups=2, zipf_s=0.8, seed=41)
+    ens.base_score = 0.25
+    x = synth.make_x(5, 7, 6).astype(np.float64)
+    np.testing.assert_allclose(parity.oracle_interactions_by_trees(ens, x, parts=4, workers=2),
+                               oracle.interactions(ens, x), rtol=0, atol=1e-13)

@@ -17,8 +17,15 @@ STUMP = [{"nodeid": 0, "depth": 0, "split": "f0", "split_condition": 0.5, "yes":
           "cover": 10, "children": [{"nodeid": 1, "leaf": 1.0, "cover": 4}, {"nodeid": 2, "leaf": 0.0, "cover": 6}]}]
 
 
-def _dump(ens):
-    """Write an ensemble as XGBoost JSON (node ids in BFS order, as XGBoost numbers them)."""
+def _dump(ens, cover_fmt=None, hess=1.0):
+    """Write an ensemble as XGBoost JSON (node ids in BFS order, as XGBoost numbers them).
+    cover_fmt: None = exact; else covers are scaled by `hess` (a hessian weight),
+    rounded to float32 (XGBoost's per-node stat type) and printed with this
+    format (e.g. "%.6g", C++ ostream's default precision)."""
+    def cv(c):
+        if cover_fmt is None:
+            return float(c)
+        return float(cover_fmt % np.float32(c * hess))
     out = []
     for t in range(ens.n_trees):
         left, right, feat, thr, cov, val = ens.tree(t)
@@ -32,10 +39,10 @@ def _dump(ens):
 
         def node(j):
             if left[j] < 0:
-                return {"nodeid": ids[j], "leaf": float(val[j]), "cover": float(cov[j])}
+                return {"nodeid": ids[j], "leaf": float(val[j]), "cover": cv(cov[j])}
             return {"nodeid": ids[j], "split": f"f{int(feat[j])}", "split_condition": float(thr[j]),
                     "yes": ids[int(left[j])], "no": ids[int(right[j])], "missing": ids[int(left[j])],
-                    "cover": float(cov[j]), "children": [node(int(left[j])), node(int(right[j]))]}
+                    "cover": cv(cov[j]), "children": [node(int(left[j])), node(int(right[j]))]}
         out.append(node(0))
     return json.dumps(out)
 
@@ -77,7 +84,9 @@ def test_errors():
     bad4 = json.loads(json.dumps(STUMP))
     bad4[0]["children"][1]["cover"] = 7
     with pytest.raises(gts.GtsError):
-        gts.gts_extract_paths(from_xgboost_dump(bad4))
+        gts.gts_extract_paths(from_xgboost_dump(bad4, covers="as_is"))
+    with pytest.raises(DumpError, match="cover"):
+        from_xgboost_dump(bad4)
 
 
 @pytest.mark.parametrize("name", ["cal_housing-med", "covtype-large"])
@@ -95,3 +104,58 @@ def test_round_trip_tables_and_values(name):
     assert np.array_equal(ref.zero_fraction, b["zero_fraction"])
     x = w.x(16, ens=ens).astype(np.float64)
     np.testing.assert_array_equal(oracle.treeshap(m, x), oracle.treeshap(ens, x))
+
+
+@pytest.mark.parametrize("fmt", ["%.6g", "%.9g"])
+def test_float32_covers_printed_at_limited_precision(fmt):
+    """Real dumps: covers are float32 hessian sums printed at 6-9 significant
+    digits, so parent != left + right beyond the library's 1e-6 check
+    (SPEC.md:35).  covers="as_is" is rejected by the library when it does not
+    conserve; "conserve" rebuilds internal covers from the leaves and the
+    values move by no more than the cover rounding."""
+    w = WORKLOADS["adult-large"]
+    ens = w.ensemble().subset(range(40))
+    doc = _dump(ens, fmt, hess=0.2371)
+    raw = from_xgboost_dump(doc, n_features=w.n_features, covers="as_is")
+    worst = 0.0
+    for t in range(raw.n_trees):
+        l, r, _, _, c, _ = raw.tree(t)
+        inner = l >= 0
+        worst = max(worst, float(np.max(np.abs(c[l[inner]] + c[r[inner]] - c[inner]) / c[inner])))
+    if worst > 1e-6:
+        with pytest.raises(gts.GtsError) as e:
+            gts.gts_extract_paths(raw)
+        assert e.value.status == 2
+    m = from_xgboost_dump(doc, n_features=w.n_features)
+    assert 0 < m.cover_adjust < 1e-5
+    gts.gts_extract_paths(m)  # validates
+    x = w.x(24, ens=ens).astype(np.float64)
+    ref = oracle.treeshap(ens, x)
+    got = oracle.treeshap(m, x)
+    s = np.abs(ref[:, :, :-1]).max(axis=2, keepdims=True)
+    assert np.all(np.abs(got - ref) <= 1e-4 * s + 1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,trees,fmt", [("covtype-large", 96, "%.6g"), ("adult-large", 60, "%.9g")])
+def test_ingested_dump_through_the_kernels(gpu, name, trees, fmt):
+    """An XGBoost-format dump (float32 covers printed at limited precision)
+    parsed by from_xgboost_dump runs through gts_shap and the fused
+    gts_shap_and_interactions call; both match O5 / O6 of the parsed model."""
+    import torch
+
+    from paper_2010_13972_b200 import TreeShapExplainer
+    from tests import parity
+    w = WORKLOADS[name]
+    ens = w.ensemble().subset(range(trees))
+    m = from_xgboost_dump(_dump(ens, fmt, hess=0.2371), num_class=w.n_groups, n_features=w.n_features)
+    x = w.x(300, ens=ens)
+    ex = TreeShapExplainer(m, device=torch.device("cuda:0"))
+    xd = torch.from_numpy(x).cuda()
+    phi = ex.shap_device(xd).cpu().numpy()
+    x64 = x.astype(np.float64)
+    parity.check(phi, oracle.treeshap(m, x64), "f32", f"{name} ingested shap")
+    pf, pij = ex.shap_and_interactions_device(xd[:12])
+    torch.cuda.synchronize()
+    parity.check(pf.cpu().numpy(), oracle.treeshap(m, x64[:12]), "f32", f"{name} ingested fused shap")
+    parity.check(pij.cpu().numpy(), oracle.interactions(m, x64[:12]), "f32", f"{name} ingested interactions")
