@@ -3,17 +3,23 @@ values), with roofline fraction, CPU-oracle baseline, clocks and an end-to-end
 number through the public API.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload cal_housing-med] [--rows-per-gpu 1048576] [--mode both|shap|interactions]
+                    [--workload covtype-large] [--mode shap|interactions|both]
+                    [--rows-per-gpu 1048576] [--rows-per-step 262144]
 
-One "step" = one pass of the per-row hot path over this rank's batch of rows
-producing the SHAP values + bias and the interaction values: in mode "both"
-one gts_shap_and_interactions call (the interaction kernel also writes phi;
-`--separate` times gts_shap + gts_shap_interactions instead, which the line
-reports beside it as "both.separate_*", and "shap" / "interactions" time each
-kernel alone), with the packed path table resident (extract -> pack -> blob runs once per model,
-PAPER.md:528, and is reported as `preprocess_ms`).  Rows are sharded across
-ranks (weak scaling); the blob is replicated by ONE NCCL broadcast.  Rank 0
-prints one JSON line.
+Default workload: BASELINE.json configs[4], covtype-large (8 classes x 1000
+rounds, depth 16, 54 features) over a 2^20-row dataset per GPU, SHAP values
+(PAPER.md:544 is the paper's number for this model; PAPER.md:584-601 its
+row-sharded scaling).  The dataset is resident in HBM; one "step" = one
+gts_shap call over the next 2^18-row window of it (windows rotate, so 4 steps
+cover the 2^20 rows): a full step at 2^20 rows would take ~40 s and 25 of them
+would not fit the driver's time limit.  Mode "interactions" times
+gts_shap_interactions, mode "both" one gts_shap_and_interactions call (phi read
+off the interaction pass; `--separate` times the two calls instead).  The
+packed path table is resident (extract -> pack -> blob runs once per model,
+PAPER.md:528; reported as `preprocess_ms` and in the cold `e2e_cold`).  Rows
+are sharded across ranks (weak scaling); rank 0 alone builds the blob and ONE
+NCCL broadcast replicates it.  At N=1 the line also carries `extra` results
+for cal_housing-med and adult-large (mode both).  Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -46,9 +52,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="cal_housing-med")
-    ap.add_argument("--rows-per-gpu", type=int, default=1 << 20)
-    ap.add_argument("--mode", choices=["both", "shap", "interactions"], default="both")
+    ap.add_argument("--workload", default="covtype-large")
+    ap.add_argument("--rows-per-gpu", type=int, default=1 << 20, help="rows of the resident dataset per GPU")
+    ap.add_argument("--rows-per-step", type=int, default=1 << 18,
+                    help="rows per timed step; steps rotate through windows of the dataset (0 = all rows)")
+    ap.add_argument("--mode", choices=["both", "shap", "interactions"], default="shap")
+    ap.add_argument("--extras", default="auto",
+                    help="comma list workload:mode:rows timed after the main run at N=1 "
+                         "('auto' = cal_housing-med:both:1048576,adult-large:both:65536; 'none')")
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
     ap.add_argument("--layout", choices=["nodal", "warp_bins"], default="nodal")
     ap.add_argument("--pack", default="bfd")
@@ -250,11 +261,145 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ ours
 
+FFMA_MEASURED_TFLOPS = 70.7  # scripts/fma_peak.cu on a B200 at 1965 MHz (profiles/r01c): scalar FFMA chains
+
+
+def _windows(n: int, per_step: int):
+    per = n if per_step <= 0 else min(per_step, n)
+    return [(r0, min(n, r0 + per)) for r0 in range(0, n, per)]
+
+
+class Runner:
+    """One workload on this rank: resident X, output buffers, the timed call."""
+
+    def __init__(self, args, w, ex, mode, n, per_step, dev, rank, separate=False):
+        import torch
+        self.args, self.w, self.ex, self.mode, self.n, self.dev = args, w, ex, mode, n, dev
+        self.G, self.M = w.n_groups, w.n_features
+        self.windows = _windows(n, per_step)
+        self.rows_per_step = self.windows[0][1] - self.windows[0][0]
+        self.fused = mode == "both" and not separate
+        self.do_shap = mode in ("both", "shap")
+        self.do_int = mode in ("both", "interactions")
+        ens = w.ensemble() if w.tie_frac > 0 else None
+        x_host = w.x(n, row0=rank * n, ens=ens)
+        self.xh = x_host if args.dtype == "f32" else x_host.astype(np.float64)
+        self.tdt = torch.float32 if args.dtype == "f32" else torch.float64
+        self.esz = 4 if args.dtype == "f32" else 8
+        if args.x_layout == "feature":  # [n][M] view of a feature-major [M][n] buffer
+            self.xt = torch.from_numpy(np.ascontiguousarray(self.xh.T)).t()
+        else:
+            self.xt = torch.from_numpy(self.xh)
+        self.xd = self.xt.to(dev)
+        from paper_2010_13972_b200.explainer import TreeShapExplainer
+        self.x_rs, self.x_cs = TreeShapExplainer._strides(self.xd)
+        G, M = self.G, self.M
+        W = self.rows_per_step
+        self.phi = torch.empty((W, G, M + 1), dtype=self.tdt, device=dev) if self.do_shap else None
+        # wide models (fashion_mnist: 24.6 MB of phi_ij per row) stream the rows in
+        # chunks through one reused buffer (SURVEY §8(f)-3); otherwise one call
+        self.ij_row_bytes = G * (M + 1) ** 2 * self.esz
+        self.ij_chunk = W if not self.do_int else max(1, min(W, (args.phi_ij_budget_gb << 30) // self.ij_row_bytes))
+        self.phi_ij = (torch.empty((self.ij_chunk, G, M + 1, M + 1), dtype=self.tdt, device=dev)
+                       if self.do_int else None)
+        self.stream = torch.cuda.current_stream(dev)
+
+    def call(self, i, evs=None):
+        """Step i: the hot path over window i mod n_windows; evs[0]/evs[1] bracket it."""
+        from paper_2010_13972_b200 import gts
+        r0, r1 = self.windows[i % len(self.windows)]
+        ex, st = self.ex, self.stream.cuda_stream
+        if evs:
+            evs[0].record(self.stream)
+        if self.fused:
+            for c0 in range(r0, r1, self.ij_chunk):
+                c1 = min(r1, c0 + self.ij_chunk)
+                xr = self.xd[c0:c1]
+                gts.gts_shap_and_interactions(ex.blob_int.info, ex.blob_int.ptr, xr.data_ptr(), c1 - c0, self.x_rs,
+                                              self.x_cs, self.phi[c0 - r0:c1 - r0].data_ptr(), self.phi_ij.data_ptr(),
+                                              st)
+        else:
+            if self.do_shap:
+                xr = self.xd[r0:r1]
+                gts.gts_shap_strided(ex.blob.info, ex.blob.ptr, xr.data_ptr(), r1 - r0, self.x_rs, self.x_cs,
+                                     self.phi.data_ptr(), st)
+            if self.do_int:
+                for c0 in range(r0, r1, self.ij_chunk):
+                    c1 = min(r1, c0 + self.ij_chunk)
+                    xr = self.xd[c0:c1]
+                    gts.gts_shap_interactions_strided(ex.blob_int.info, ex.blob_int.ptr, xr.data_ptr(), c1 - c0,
+                                                      self.x_rs, self.x_cs, self.phi_ij.data_ptr(), st)
+        if evs:
+            evs[1].record(self.stream)
+        return r1 - r0
+
+    def launches_per_step(self):
+        from paper_2010_13972_b200 import gts
+        n_chunks = -(-self.rows_per_step // self.ij_chunk)
+        if self.fused:
+            return gts.gts_launches_per_call(self.ex.blob_int.info, 2) * n_chunks
+        return ((gts.gts_launches_per_call(self.ex.blob.info, False) if self.do_shap else 0) +
+                (gts.gts_launches_per_call(self.ex.blob_int.info, True) * n_chunks if self.do_int else 0))
+
+    def timed(self, steps, warmup, flush, world, clk=None):
+        """W untimed + K timed steps (L2 flushed before each, outside the events);
+        returns per-step device ms (CUDA events on the launch stream) and rows."""
+        import torch
+        for i in range(warmup):
+            self.call(i)
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        ms, rows = [], []
+        for i in range(steps):
+            flush.zero_()
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            rows.append(self.call(warmup + i, evs))
+            torch.cuda.synchronize()
+            ms.append(evs[0].elapsed_time(evs[1]))
+        torch.cuda.synchronize()
+        barrier(world)
+        return ms, rows
+
+    def flops_per_row(self):
+        if self.mode == "shap":
+            info = self.ex.blob.info
+            return info.shap_flops_per_row, info.paper_shap_flops_per_row
+        info = self.ex.blob_int.info
+        return info.inter_flops_per_row, info.paper_inter_flops_per_row
+
+
+def roofline(flops_per_row, paper_flops_per_row, rows, ms, peak, f_med_over_max):
+    """Dominant kernel's roofline: FP32-ALU bound; achieved =
+    algorithmic flops per launch / event time.  frac_nodal counts what the
+    nodal formulation computes (gts_blob_info.*_flops_per_row, DESIGN R1);
+    frac_survey_8d counts SURVEY §8(d)'s op count of the paper's recurrence
+    (it exceeds 1 when the nodal form needs fewer operations)."""
+    if ms <= 0:
+        return None
+    ach = flops_per_row * rows / (ms / 1000.0) / 1e12
+    paper = paper_flops_per_row * rows / (ms / 1000.0) / 1e12
+    return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "frac_nodal": ach / peak, "frac_survey_8d": paper / peak,
+            "peak_kind": "nominal: SMs x 128 FP32 lanes x 2 x max SM clock",
+            "peak_ffma_measured": FFMA_MEASURED_TFLOPS, "frac_vs_ffma_measured": ach / FFMA_MEASURED_TFLOPS,
+            "frac_at_median_clock": ach / (peak * f_med_over_max), "traffic": None,
+            "flops_per_row": flops_per_row, "paper_flops_per_row": paper_flops_per_row,
+            "survey_8d_equiv_tflops": paper}
+
+
+def _traffic_entry(workload, layout, mode, dtype):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(path)).get(f"{workload}/{layout}/{mode}/{dtype}")
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
 
-    from paper_2010_13972_b200 import gts
-    from paper_2010_13972_b200.explainer import Blob, TreeShapExplainer
+    from paper_2010_13972_b200.explainer import TreeShapExplainer
     from synth.configs import WORKLOADS
 
     world, rank, local = dist_setup(args)
@@ -263,201 +408,154 @@ def run_ours(args):
     ens = w.ensemble()
     M, G = w.n_features, w.n_groups
     n = int(args.rows_per_gpu)
-    do_shap = args.mode in ("both", "shap")
-    do_int = args.mode in ("both", "interactions")
+    mode = args.mode
+    fused = mode == "both" and not args.separate
+    kw = dict(dtype=args.dtype, pack=args.pack, layout=args.layout, device=dev, max_slots=args.max_slots)
 
-    # --- model preprocessing: rank 0 extracts + packs + writes the blob; one broadcast
+    # --- model preprocessing: rank 0 extracts + packs + writes the blob the mode
+    #     needs; ONE broadcast replicates it (TreeShapExplainer.replicated)
     t0 = time.perf_counter()
-    if rank == 0:
-        ex = TreeShapExplainer(ens, dtype=args.dtype, pack=args.pack, layout=args.layout, device=dev,
-                               interactions=do_int, max_slots=args.max_slots)
+    if world > 1:
+        barrier(world)
+        ex = TreeShapExplainer.replicated(ens, mode=("both" if fused else mode) if not args.separate else mode,
+                                          **kw)
+        if args.separate and mode == "both":
+            _ = ex.blob  # --separate needs the SHAP blob too (not part of the one-broadcast setup)
     else:
-        ex = TreeShapExplainer(ens, dtype=args.dtype, pack=args.pack, layout=args.layout, device=dev,
-                               interactions=do_int, build_blobs=False, max_slots=args.max_slots)
-        ex.blob = Blob(None, torch.empty(0, dtype=torch.uint8, device=dev))
-        ex.blob_int = Blob(None, torch.empty(0, dtype=torch.uint8, device=dev)) if do_int else None
+        ex = TreeShapExplainer(ens, interactions=False, build_blobs=False, **kw)
+        if mode in ("shap",) or (mode == "both" and args.separate):
+            _ = ex.blob
+        if mode in ("interactions", "both"):
+            _ = ex.blob_int
     torch.cuda.synchronize()
     pre_ms = 1000 * (time.perf_counter() - t0)
-    bcast_ms = 0.0
-    if world > 1:
-        # every rank knows whether the interaction kernel reuses the SHAP blob
-        same = args.layout == "warp_bins" or M <= 16
-        barrier(world)
-        t1 = time.perf_counter()
-        ex.blob.broadcast(0)
-        if do_int:
-            ex.blob_int = ex.blob if same else ex.blob_int.broadcast(0)
-        torch.cuda.synchronize()
-        bcast_ms = 1000 * (time.perf_counter() - t1)
-    info_s, info_i = ex.blob.info, (ex.blob_int.info if do_int else None)
-    bins_view = ex.bins.view()
+    timings = dict(ex.timings)
+    bcast_ms = 1000 * timings.get("broadcast_s", 0.0)
+    info_main = ex.blob.info if mode == "shap" else ex.blob_int.info
+    bins_view = ex.bins.view() if ex.bins is not None else None
 
-    # --- this rank's rows (counter-keyed generator: no scatter)
-    x_host = w.x(n, row0=rank * n, ens=ens if w.tie_frac > 0 else None)
-    xh = x_host if args.dtype == "f32" else x_host.astype(np.float64)
-    if args.x_layout == "feature":  # [n][M] view of a feature-major [M][n] buffer
-        xt = torch.from_numpy(np.ascontiguousarray(xh.T)).t()
-    else:
-        xt = torch.from_numpy(xh)
-    xd = xt.to(dev)
-    x_rs, x_cs = TreeShapExplainer._strides(xd)
-    tdt = torch.float32 if args.dtype == "f32" else torch.float64
-    phi = torch.empty((n, G, M + 1), dtype=tdt, device=dev) if do_shap else None
-    # wide models (fashion_mnist: 24.6 MB of phi_ij per row) stream the rows in
-    # chunks through one reused buffer; otherwise one call
-    ij_row_bytes = G * (M + 1) ** 2 * (4 if args.dtype == "f32" else 8)
-    ij_chunk = n if not do_int else max(1, min(n, (args.phi_ij_budget_gb << 30) // ij_row_bytes))
-    phi_ij = torch.empty((ij_chunk, G, M + 1, M + 1), dtype=tdt, device=dev) if do_int else None
+    run = Runner(args, w, ex, mode, n, args.rows_per_step, dev, rank, separate=args.separate)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
-
-    fused = args.mode == "both" and not args.separate
-
-    def fused_step(evs=None):
-        if evs: evs[4].record(stream)
-        for r0 in range(0, n, ij_chunk):
-            xr = xd[r0:r0 + ij_chunk]
-            gts.gts_shap_and_interactions(info_i, ex.blob_int.ptr, xr.data_ptr(), xr.shape[0], x_rs, x_cs,
-                                          phi[r0:r0 + ij_chunk].data_ptr(), phi_ij.data_ptr(), stream.cuda_stream)
-        if evs: evs[5].record(stream)
-
-    def step(evs=None):
-        if do_shap:
-            if evs: evs[0].record(stream)
-            gts.gts_shap_strided(info_s, ex.blob.ptr, xd.data_ptr(), n, x_rs, x_cs, phi.data_ptr(),
-                                 stream.cuda_stream)
-            if evs: evs[1].record(stream)
-        if do_int:
-            if evs: evs[2].record(stream)
-            for r0 in range(0, n, ij_chunk):
-                xr = xd[r0:r0 + ij_chunk]
-                gts.gts_shap_interactions_strided(info_i, ex.blob_int.ptr, xr.data_ptr(), xr.shape[0], x_rs, x_cs,
-                                                  phi_ij.data_ptr(), stream.cuda_stream)
-            if evs: evs[3].record(stream)
-
-    for _ in range(args.warmup):
-        step()
-        if fused:
-            fused_step()
-    torch.cuda.synchronize()
     gpu_uuid = str(torch.cuda.get_device_properties(dev).uuid)
     gpu_id = gpu_uuid if gpu_uuid.startswith("GPU-") else "GPU-" + gpu_uuid
-    t_step, t_shap, t_int, t_sep = [], [], [], []
-    barrier(world)
-    torch.cuda.synchronize()
     with ClockSampler(gpu_id) as clk:
-        for _ in range(args.steps):
-            flush.zero_()  # L2 flush between timed steps (outside the events)
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-            step(evs)
-            if fused:
-                flush.zero_()
-                fused_step(evs)
-            torch.cuda.synchronize()
-            ts = evs[0].elapsed_time(evs[1]) if do_shap else 0.0
-            ti = evs[2].elapsed_time(evs[3]) if do_int else 0.0
-            t_shap.append(ts)
-            t_int.append(ti)
-            t_sep.append(ts + ti)
-            t_step.append(evs[4].elapsed_time(evs[5]) if fused else ts + ti)
-    torch.cuda.synchronize()
-    barrier(world)
-    ms_step = max_over_ranks(float(np.mean(t_step)), world)
-    ms_sep = max_over_ranks(float(np.mean(t_sep)), world)
-    ms_shap = max_over_ranks(float(np.mean(t_shap)), world)
-    ms_int = max_over_ranks(float(np.mean(t_int)), world)
+        ms, rows = run.timed(args.steps, args.warmup, flush, world)
     clocks = clk.summary()
+    ms_step = max_over_ranks(float(np.mean(ms)), world)
+    ms_med = max_over_ranks(float(np.median(ms)), world)
+    ms_min = max_over_ranks(float(np.min(ms)), world)
+    rows_step = int(np.mean(rows))
 
-    # --- end to end through the public API: pinned host X -> device -> host phi
-    e2e = None
+    # --- end to end through the public API: pinned host X -> device -> host outputs
+    e2e = e2e_cold = None
     if not args.no_e2e:
-        x_pin = xt.pin_memory()
-        phi_h = torch.empty(phi.shape, dtype=tdt, pin_memory=True) if do_shap else None
-        e2e_chunk = max(1, min(ij_chunk, (4 << 30) // ij_row_bytes))  # pinned host staging <= 4 GiB
-        phi_ij_h = torch.empty((e2e_chunk,) + tuple(phi_ij.shape[1:]), dtype=tdt, pin_memory=True) if do_int else None
-        xe = torch.empty_like(xd)
-
-        pipelined = not args.e2e_serial and ij_chunk == n and args.x_layout == "row"
-        if pipelined:
-            phi_ij_h = torch.empty(tuple(phi_ij.shape), dtype=tdt, pin_memory=True) if do_int else None
-            del phi_ij  # the pipelined call has its own device slots
+        W = run.rows_per_step
+        x_pin = run.xt.pin_memory()  # the whole dataset: every window's H2D reads pinned memory
+        phi_h = torch.empty((W, G, M + 1), dtype=run.tdt, pin_memory=True) if run.do_shap else None
+        phi_ij_h = None
+        pipelined = not args.e2e_serial and run.ij_chunk == W and args.x_layout == "row"
+        if run.do_int:
+            rows_h = W if pipelined else run.ij_chunk
+            phi_ij_h = torch.empty((min(rows_h, max(1, (4 << 30) // run.ij_row_bytes)), G, M + 1, M + 1),
+                                   dtype=run.tdt, pin_memory=True)
+            if phi_ij_h.shape[0] < W:
+                pipelined = False
+        if pipelined and run.phi_ij is not None:
+            run.phi_ij = None  # the pipelined call has its own device slots
             torch.cuda.empty_cache()
+        xe = torch.empty((W, run.xd.shape[1]), dtype=run.tdt, device=dev)
+        stream = run.stream
 
-        def e2e_step():
+        def e2e_step(i):
+            r0, r1 = run.windows[i % len(run.windows)]
+            m = r1 - r0
             if pipelined:
-                ex.explain_host_pipelined(x_pin, phi_h, phi_ij_h, chunk_rows=max(1, -(-n // args.e2e_chunks)))
-                return
-            xe.copy_(x_pin, non_blocking=True)
+                ex.explain_host_pipelined(x_pin[r0:r1], phi_h[:m] if run.do_shap else None,
+                                          phi_ij_h[:m] if run.do_int else None,
+                                          chunk_rows=max(1, -(-m // args.e2e_chunks)))
+                return m
+            xe[:m].copy_(x_pin[r0:r1], non_blocking=True)
             if fused:
-                for r0 in range(0, n, e2e_chunk):
-                    r1 = min(n, r0 + e2e_chunk)
-                    ex.shap_and_interactions_device(xe[r0:r1], out_phi=phi[r0:r1], out_phi_ij=phi_ij[: r1 - r0],
-                                                    stream=stream)
-                    phi_ij_h[: r1 - r0].copy_(phi_ij[: r1 - r0], non_blocking=True)
-                phi_h.copy_(phi, non_blocking=True)
-                return
-            if do_shap:
-                ex.shap_device(xe, out=phi, stream=stream)
-                phi_h.copy_(phi, non_blocking=True)
-            if do_int:
-                for r0, r1, chunk in ex.iter_interactions(xe, e2e_chunk, stream=stream, n_buffers=1):
-                    phi_ij_h[: r1 - r0].copy_(chunk, non_blocking=True)
+                for c0 in range(0, m, phi_ij_h.shape[0]):
+                    c1 = min(m, c0 + phi_ij_h.shape[0])
+                    pf, pij = ex.shap_and_interactions_device(xe[c0:c1], stream=stream)
+                    phi_ij_h[:c1 - c0].copy_(pij, non_blocking=True)
+                    phi_h[c0:c1].copy_(pf, non_blocking=True)
+                return m
+            if run.do_shap:
+                ex.shap_device(xe[:m], out=run.phi[:m], stream=stream)
+                phi_h[:m].copy_(run.phi[:m], non_blocking=True)
+            if run.do_int:
+                for c0, c1, chunk in ex.iter_interactions(xe[:m], phi_ij_h.shape[0], stream=stream, n_buffers=1):
+                    phi_ij_h[:c1 - c0].copy_(chunk, non_blocking=True)
+            return m
 
-        for _ in range(2):
-            e2e_step()
+        # cold: the first call of a fresh model = preprocessing + one e2e step
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        m0 = e2e_step(0)
+        b.record(stream)
+        torch.cuda.synchronize()
+        first_ms = a.elapsed_time(b)
+        e2e_step(1)
         torch.cuda.synchronize()
         barrier(world)
-        te = []
-        for _ in range(max(2, args.steps // 2)):
+        te, tr = [], []
+        reps = max(2, min(args.steps // 2, 5))
+        for i in range(reps):
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            e2e_step()
+            tr.append(e2e_step(i))
             b.record(stream)
             torch.cuda.synchronize()
             te.append(a.elapsed_time(b))
         ms_e2e = max_over_ranks(float(np.mean(te)), world)
-        h2d = xt.numel() * xt.element_size()
-        d2h = (phi.numel() * phi.element_size() if do_shap else 0) + (n * ij_row_bytes if do_int else 0)
-        e2e = {"value": world * n / (ms_e2e / 1000.0), "unit": "rows/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e,
+        rows_e2e = float(np.mean(tr))
+        h2d = int(rows_e2e * M * run.esz)
+        d2h = int(rows_e2e * ((G * (M + 1) * run.esz if run.do_shap else 0) + (run.ij_row_bytes if run.do_int else 0)))
+        e2e = {"value": world * rows_e2e / (ms_e2e / 1000.0), "unit": "rows/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e, "steps": reps,
                "api": (f"TreeShapExplainer.explain_host_pipelined (pinned host X -> {args.e2e_chunks} chunks on "
-                       "3 streams, H2D / kernel / D2H overlapped -> pinned host phi and phi_ij)" if pipelined else
+                       "3 streams, H2D / kernel / D2H overlapped -> pinned host outputs)" if pipelined else
                        ("TreeShapExplainer.shap_and_interactions_device" if fused else
                         "TreeShapExplainer.shap_device/interactions_device") +
-                       " with pinned host X and phi (H2D + D2H)")}
+                       " with pinned host X and outputs (H2D + D2H)")}
+        cold_s = pre_ms / 1000.0 + first_ms / 1000.0
+        e2e_cold = {"value": world * m0 / cold_s, "unit": "rows/s", "rows": m0, "seconds": cold_s,
+                    "preprocess_s": pre_ms / 1000.0, "first_call_s": first_ms / 1000.0,
+                    "breakdown_s": {k: round(v, 4) for k, v in timings.items()},
+                    "note": "fresh model: extract + pack + plan + blob write + H2D (+ broadcast) + one e2e step "
+                            "(SURVEY §8(d) end to end)"}
 
     # --- ablation: the paper-lineage warp-bin kernels on a slice of the rows
     ablation = None
-    if not args.no_ablation and rank == 0:
-        # the paper-lineage warp-bin kernels on a slice of the rows; with
-        # --pack-ablation every packer's bins (utilisation ->
-        # kernel time), SHAP only
-        na = min(n, args.ablation_rows)
-        xa = xd[:na]
+    if not args.no_ablation and rank == 0 and world == 1:
+        na = min(run.rows_per_step, args.ablation_rows)
+        xa = run.xd[:na]
         res = {"rows": na, "layout": "warp_bins (paper lineage: lane per path element, shuffles, swap-to-end)"}
 
-        def timed(fn, x):
+        def timed1(fn, x):
             fn(x)
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
+            a.record(run.stream)
             fn(x)
-            b.record(stream)
+            b.record(run.stream)
             torch.cuda.synchronize()
             return x.shape[0] / (a.elapsed_time(b) / 1000.0)
 
         packs = ["bfd", "ffd", "nf", "none"] if args.pack_ablation else [args.pack]
         for pk in packs:
             exb = TreeShapExplainer(ens, dtype=args.dtype, pack=pk, layout="warp_bins", device=dev,
-                                    interactions=do_int and pk == args.pack)
+                                    interactions=run.do_int and pk == args.pack)
             bv = exb.bins.view()
             ent = {"bins": int(bv["n_bins"]), "utilisation": bv["utilisation"]}
-            if do_shap:
-                ent["shap_rows_per_s"] = timed(exb.shap_device, xa)
-            if do_int and pk == args.pack:
-                ni = max(1, min(na, ij_chunk, 8192))
-                ent["interactions_rows_per_s"] = timed(exb.interactions_device, xa[:ni])
+            if run.do_shap:
+                ent["shap_rows_per_s"] = timed1(exb.shap_device, xa)
+            if run.do_int and pk == args.pack:
+                ni = max(1, min(na, run.ij_chunk, 8192))
+                ent["interactions_rows_per_s"] = timed1(exb.interactions_device, xa[:ni])
                 ent["interaction_rows"] = ni
             if pk == args.pack:
                 res.update(ent)
@@ -466,16 +564,6 @@ def run_ours(args):
             del exb
         ablation = res
 
-    cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_rates(w, ens, args.mode, args.cpu_seconds)
-
-    if rank != 0:
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
-        return
-
     peaks = measured_peaks()
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     f_max = (clocks["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)) * 1e6
@@ -483,43 +571,44 @@ def run_ours(args):
     fp32_peak = sm_count * FP32_LANES_PER_SM * 2 * f_max / 1e12  # TFLOP/s
     if args.dtype == "f64":
         fp32_peak /= 2.0  # B200: FP64 at half the FP32 rate
-    total_rows = world * n
+    fpr, ppr = run.flops_per_row()
+    roof = roofline(fpr, ppr, rows_step, ms_step, fp32_peak, f_med / f_max)
+    roof["kernel"] = {"shap": "gts_shap", "interactions": "gts_shap_interactions",
+                      "both": "gts_shap_and_interactions" if fused else "gts_shap + gts_shap_interactions"}[mode] + \
+        f" ({args.layout} kernel + init fill, CUDA events on the launch stream)"
+    roof["ms_median"], roof["ms_min"] = ms_med, ms_min
+    tr = _traffic_entry(args.workload, args.layout, mode, args.dtype)
+    if tr:
+        rows_prof = tr.get("rows_per_launch")
+        scale = (rows_step / rows_prof) if rows_prof else 1.0
+        roof["traffic"] = tr.get("dram_bytes_per_launch") * scale
+        roof["traffic_source"] = tr.get("source") + (f" (captured at {rows_prof} rows, scaled to {rows_step})"
+                                                     if rows_prof and rows_prof != rows_step else "")
+        if tr.get("executed_fp32_flops_per_row"):
+            roof["ncu_executed_fp32_flops_per_row"] = tr["executed_fp32_flops_per_row"]
+            roof["ncu_executed_over_nodal"] = tr["executed_fp32_flops_per_row"] / fpr
+    roof["algorithmic_bytes_per_row"] = (M * run.esz + (G * (M + 1) * run.esz if run.do_shap else 0) +
+                                         (run.ij_row_bytes if run.do_int else 0) + info_main.bytes / rows_step)
 
-    def roof(flops_per_row, paper_flops_per_row, ms):
-        if ms <= 0:
-            return None
-        ach = flops_per_row * n / (ms / 1000.0) / 1e12
-        return {"bound": "alu", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s", "frac": ach / fp32_peak,
-                "frac_at_median_clock": ach / (fp32_peak * f_med / f_max), "traffic": None,
-                "flops_per_row": flops_per_row,
-                "paper_recurrence_equiv_tflops": paper_flops_per_row * n / (ms / 1000.0) / 1e12}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_rates(w, ens, mode, args.cpu_seconds)
 
-    r_shap = roof(info_s.shap_flops_per_row, info_s.paper_shap_flops_per_row, ms_shap) if do_shap else None
-    r_int = roof(info_i.inter_flops_per_row, info_i.paper_inter_flops_per_row, ms_int) if do_int else None
-    dominant = "interactions" if (do_int and ms_int >= ms_shap) else "shap"
-    if fused:
-        # the step is the fused call: the interaction kernel's work, phi read off its diagonal
-        r_both = roof(info_i.inter_flops_per_row, info_i.paper_inter_flops_per_row, ms_step)
-        roofline = dict(r_both)
-        roofline["kernel"] = (f"gts_shap_and_interactions ({args.layout} interaction kernel writing phi and phi_ij "
-                              "+ init fills, CUDA events on the launch stream)")
-    else:
-        roofline = dict((r_int if dominant == "interactions" else r_shap) or {})
-        roofline["kernel"] = ("gts_shap_interactions" if dominant == "interactions" else "gts_shap") + \
-            f" ({args.layout} kernel + init fill, CUDA events on the launch stream)"
-    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(traffic_file):
-        try:
-            tr = json.load(open(traffic_file)).get(
-                f"{args.workload}/{args.layout}/{'both' if fused else dominant}/{args.dtype}")
-            if tr:
-                roofline["traffic"] = tr.get("dram_bytes_per_launch")
-                roofline["traffic_source"] = tr.get("source")
-        except Exception:
-            pass
-    launches_sep = (gts.gts_launches_per_call(info_s, False) if do_shap else 0) + (
-        gts.gts_launches_per_call(info_i, True) * -(-n // ij_chunk) if do_int else 0)
-    launches = gts.gts_launches_per_call(info_i, 2) * -(-n // ij_chunk) if fused else launches_sep
+    extras = None
+    if world == 1 and rank == 0 and args.extras != "none":
+        spec = ("cal_housing-med:both:1048576,adult-large:both:65536" if args.extras == "auto" else args.extras)
+        extras = {}
+        for item in spec.split(","):
+            name, xmode, xrows = item.split(":")
+            extras[f"{name}:{xmode}"] = run_extra(args, name, xmode, int(xrows), dev, flush, fp32_peak, f_med / f_max)
+
+    launches = run.launches_per_step()
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    total_rows = world * rows_step
     line = {
         "metric": METRIC,
         "value": total_rows / (ms_step / 1000.0),
@@ -528,44 +617,77 @@ def run_ours(args):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_step,
+        "ms_per_step_median": ms_med,
+        "ms_per_step_min": ms_min,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": args.dtype,
         "data": "synthetic",
-        "config": {"workload": args.workload, "mode": args.mode, "rows_per_gpu": n, "global_rows": total_rows,
+        "config": {"workload": args.workload, "mode": mode, "rows_per_gpu": n, "rows_per_step": rows_step,
+                   "global_rows_per_step": total_rows, "windows": len(run.windows),
+                   "steps_note": "each step explains the next rows_per_step-row window of the resident "
+                                 "rows_per_gpu-row dataset (windows rotate)",
                    "trees": w.n_trees, "max_depth": w.max_depth, "features": M, "groups": G,
-                   "paths": int(info_s.n_paths), "path_elems": int(info_s.n_elems), "layout": args.layout,
-                   "pack": args.pack, "x_layout": args.x_layout, "max_slots": int(info_s.max_slots), "bins": int(bins_view["n_bins"]),
-                   "bin_utilisation": round(float(bins_view["utilisation"]), 6),
-                   "phi_ij_chunk_rows": ij_chunk if do_int else None,
-                   "l2": "flushed between timed steps (512 MiB memset outside the events); phi_ij > L2",
+                   "paths": int(info_main.n_paths), "path_elems": int(info_main.n_elems), "layout": args.layout,
+                   "pack": args.pack, "x_layout": args.x_layout, "max_slots": int(info_main.max_slots),
+                   "blob_bytes": int(info_main.bytes),
+                   "bins": int(bins_view["n_bins"]) if bins_view else None,
+                   "bin_utilisation": round(float(bins_view["utilisation"]), 6) if bins_view else None,
+                   "phi_ij_chunk_rows": run.ij_chunk if run.do_int else None,
+                   "l2": "flushed between timed steps (512 MiB memset outside the events)",
                    "parallelism": f"dp{world}: rows sharded, path table replicated by one NCCL broadcast"},
-        "shap": {"rows_per_s": total_rows / (ms_shap / 1000.0), "ms": ms_shap, "roofline": r_shap} if do_shap else None,
-        "interactions": {"rows_per_s": total_rows / (ms_int / 1000.0), "ms": ms_int, "roofline": r_int}
-        if do_int else None,
-        "both": ({"rows_per_s": total_rows / (ms_step / 1000.0), "ms": ms_step,
-                  "call": "gts_shap_and_interactions (one pass: phi and phi_ij)",
-                  "separate_rows_per_s": total_rows / (ms_sep / 1000.0), "separate_ms": ms_sep,
-                  "separate_launches_per_step": launches_sep} if fused else None),
-        "roofline": roofline,
+        "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_cold": e2e_cold,
         "gpu_launches": launches * args.steps,
         "gpu_launches_per_step": launches,
         "clocks": clocks,
         "preprocess_ms": pre_ms,
-        "pack_seconds": bins_view["pack_seconds"],
+        "preprocess_breakdown_s": {k: round(v, 4) for k, v in timings.items()},
+        "pack_seconds": bins_view["pack_seconds"] if bins_view else None,
         "broadcast_ms": bcast_ms,
+        "extra": extras,
         "ablation_paper_kernels": ablation,
         "paper_v100_context": PAPER_V100.get(args.workload),
         "peak_source": f"FP32 {sm_count} SMs x {FP32_LANES_PER_SM} lanes x 2 x max SM clock (DESIGN.md §6); "
+                       f"FFMA microbenchmark {FFMA_MEASURED_TFLOPS} TFLOP/s (profiles/r01c); "
                        f"HBM {peaks.get('hbm_gbs')} GB/s measured",
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def run_extra(args, name, mode, rows, dev, flush, peak, f_ratio):
+    """A secondary workload at N=1 (same timing rules, 3 warm-up + 5 timed steps)."""
+    import torch
+
+    from paper_2010_13972_b200.explainer import TreeShapExplainer
+    from synth.configs import WORKLOADS
+    w = WORKLOADS[name]
+    ens = w.ensemble()
+    t0 = time.perf_counter()
+    ex = TreeShapExplainer(ens, dtype=args.dtype, pack=args.pack, layout=args.layout, device=dev,
+                           interactions=False, build_blobs=False)
+    _ = ex.blob if mode == "shap" else ex.blob_int
+    pre = time.perf_counter() - t0
+    sub = argparse.Namespace(**vars(args))
+    sub.x_layout = "row"
+    run = Runner(sub, w, ex, mode, rows, rows, dev, 0)
+    ms, rws = run.timed(5, 3, flush, 1)
+    fpr, ppr = run.flops_per_row()
+    r = roofline(fpr, ppr, rws[0], float(np.mean(ms)), peak, f_ratio)
+    out = {"rows_per_step": rws[0], "rows_per_s": rws[0] / (float(np.mean(ms)) / 1000.0), "ms": float(np.mean(ms)),
+           "ms_min": float(np.min(ms)), "frac_nodal": r["frac_nodal"], "frac_survey_8d": r["frac_survey_8d"],
+           "achieved_tflops": r["achieved"], "preprocess_s": pre,
+           "call": {"shap": "gts_shap", "interactions": "gts_shap_interactions",
+                    "both": "gts_shap_and_interactions"}[mode], "paper_v100_context": PAPER_V100.get(name)}
+    del run, ex
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_sweep(args):

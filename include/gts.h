@@ -180,7 +180,9 @@ typedef struct gts_blob_info {
   int64_t max_chunk_paths;
   int32_t uses;                 /* gts_blob_use bits the blob serves (NODAL; WARP_BINS: both) */
   int32_t n_tables;             /* NODAL: nodal table rows per element record (2 or 3) */
-  int64_t reserved[4];
+  int32_t max_chunk_slots;      /* NODAL: widest slot map of any chunk (SHAP tile row = this + 1) */
+  int32_t chunk_bytes;          /* NODAL: staged-bytes budget per chunk the plan used */
+  int64_t reserved[3];
 } gts_blob_info;
 
 /* What a blob is planned for.  NODAL blobs carry per-path nodal tables

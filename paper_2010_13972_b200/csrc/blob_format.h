@@ -19,6 +19,9 @@ constexpr int kWarp = 32;                 // bin capacity B = warp size (PAPER.m
 constexpr int kQMax = 16;                 // Gauss nodes for merged k <= 31 (k = 2Q max)
 constexpr int kMaxChunkPaths = 256;
 constexpr int kChunkBytes = 16 * 1024;    // NODAL: staged bytes per chunk (one TMA bulk copy)
+#ifndef GTS_CHUNK_BYTES_WIDE
+#define GTS_CHUNK_BYTES_WIDE (16 * 1024)  // SHAP-only blobs with identity maps of > 16 features
+#endif
 
 struct BlobHeader {            // 256 bytes at offset 0
   uint32_t magic, version;
@@ -39,7 +42,9 @@ struct BlobHeader {            // 256 bytes at offset 0
   int64_t max_chunk_paths;
   int32_t uses;                // gts_blob_use bits (NODAL: which kernels the tables serve)
   int32_t n_tables;            // NODAL: table rows per record (2: SHAP only; 3: interactions)
-  int64_t reserved[11];
+  int32_t max_chunk_slots;     // NODAL: widest slot map of any chunk
+  int32_t chunk_bytes;         // NODAL: staged-bytes budget per chunk
+  int64_t reserved[10];
 };
 static_assert(sizeof(BlobHeader) == 256, "header size");
 

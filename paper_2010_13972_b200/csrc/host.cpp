@@ -466,6 +466,7 @@ struct NodalPlan {
   std::vector<uint8_t> slots;  // slot of every planned element, chunk after chunk
   std::vector<double> work_shap, work_inter;
   int64_t max_words = 0, max_elems = 0, max_paths = 0;
+  int32_t max_slots_used = 0, chunk_bytes = kChunkBytes;
 };
 
 // Default slot width of a SHAP-only blob: identity slot map up to 64 features.
@@ -497,6 +498,9 @@ static double paper_inter_flops(int k) { return paper_shap_flops(k) + (double)k 
 static void plan_nodal(const PathTable& tab, int S, int nt, size_t tsize, NodalPlan& np) {
   const int32_t M = tab.n_features;
   const bool identity = M <= S;
+  // wide identity tiles (SHAP only) leave less shared memory for staging
+  const int chunk_bytes = (identity && S >= 32 && nt == 2) ? GTS_CHUNK_BYTES_WIDE : kChunkBytes;
+  np.chunk_bytes = chunk_bytes;
   const int64_t L = tab.n_paths();
   std::vector<uint64_t> mask;
   if (identity) {
@@ -569,7 +573,7 @@ static void plan_nodal(const PathTable& tab, int S, int nt, size_t tsize, NodalP
       if (tab.group[p] != c.group) break;
       const int k = tab.len(p) - 1, q = (k + 1) / 2;
       const int64_t w = path_bytes(k, q);
-      if (!members.empty() && bytes + w > kChunkBytes) break;
+      if (!members.empty() && bytes + w > chunk_bytes) break;
       if (!identity) {  // union of two sorted feature lists
         const int32_t* pf = &tab.feature[tab.path_offset[p] + 1];
         int a = 0, b = 0, n = 0;
@@ -642,6 +646,7 @@ static void plan_nodal(const PathTable& tab, int S, int nt, size_t tsize, NodalP
     np.max_words = std::max<int64_t>(np.max_words, c.data_bytes);
     np.max_elems = std::max<int64_t>(np.max_elems, nel);
     np.max_paths = std::max<int64_t>(np.max_paths, c.n_paths);
+    np.max_slots_used = std::max<int32_t>(np.max_slots_used, c.n_slots);
     np.chunks.push_back(c);
     np.work_shap.push_back(ws);
     np.work_inter.push_back(wi);
@@ -756,6 +761,8 @@ static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, in
     h.max_chunk_bytes = P.max_words;
     h.max_chunk_elems = P.max_elems;
     h.max_chunk_paths = P.max_paths;
+    h.max_chunk_slots = P.max_slots_used;
+    h.chunk_bytes = P.chunk_bytes;
     h.off_gauss = off;
     off = align256(off + (int64_t)tsize * kQMax * 3 * kQMax);
     h.off_units = off;
@@ -809,6 +816,8 @@ static gts_status blob_plan(const gts_bins* b, int32_t dtype, int32_t layout, in
   info->max_chunk_paths = h.max_chunk_paths;
   info->uses = h.uses;
   info->n_tables = h.n_tables;
+  info->max_chunk_slots = h.max_chunk_slots;
+  info->chunk_bytes = h.chunk_bytes;
   if (hdr) *hdr = h;
   return GTS_OK;
 }

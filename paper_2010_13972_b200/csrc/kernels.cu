@@ -162,12 +162,14 @@ size_t nodal_buffer_bytes(const gts_blob_info* info) {
   return ((size_t)info->max_chunk_bytes + 127) & ~size_t(127);
 }
 
+int shap_tile_w(const gts_blob_info* info) { return (int)((info->max_chunk_slots + 1) | 1); }
+
 template <typename T, bool kInter, int S>
 size_t nodal_smem_bytes(const gts_blob_info* info) {
   constexpr int W = nodal::Cfg<T, kInter, S>::W;
   constexpr int R = nodal::Cfg<T, kInter, S>::R;
   // tiles, then two TMA staging buffers (double buffering) and their mbarriers
-  return (size_t)nodal::staging_byte_offset<T, S, W, R, kInter>() + 2 * nodal_buffer_bytes(info) + 16;
+  return (size_t)nodal::staging_byte_offset<T, S, W, R, kInter>(shap_tile_w(info)) + 2 * nodal_buffer_bytes(info) + 16;
 }
 
 template <typename T, bool kInter, int S>
@@ -210,6 +212,7 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   a.out_phi = out_phi;
   a.upper_only = kInter && uses_mirror(info);
   a.n_splits = (int)splits;
+  a.tile_w = shap_tile_w(info);
   a.M = info->n_features;
   a.G = info->n_groups;
   a.n_chunks = info->n_units;

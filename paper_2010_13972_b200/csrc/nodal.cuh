@@ -88,6 +88,18 @@ __device__ __forceinline__ void lds_vec(T (&dst)[N], const T* src) {
   }
 }
 
+// N float2 pairs from a 16-byte aligned row (table rows are padded to 4 words):
+// LDS.128 per two pairs instead of LDS.64 per pair.
+template <int N>
+__device__ __forceinline__ void lds_pairs(float2 (&dst)[N], const float* src) {
+#pragma unroll
+  for (int h = 0; h < N; h += 2) {
+    const float4 v = *reinterpret_cast<const float4*>(src + 2 * h);
+    dst[h] = make_float2(v.x, v.y);
+    if (h + 1 < N) dst[h + 1] = make_float2(v.z, v.w);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ bool one_fraction(T x, int4 rec) {
   // o = [lower <= x < upper]  (half-open bounds, reading G1)
@@ -214,13 +226,15 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
   }
   for (int p = 0; p < n_run; ++p) {
     const int4* Ep = E + p * k;
-    const float2* tp = reinterpret_cast<const float2*>(tab + p * words);
+    const float* tp = tab + p * words;
     float2 P[R][QH];
+    {
+      float2 c[QH];
+      lds_pairs(c, tp);
 #pragma unroll
-    for (int h = 0; h < QH; ++h) {
-      const float2 c = tp[h];
+      for (int h = 0; h < QH; ++h)
 #pragma unroll
-      for (int r = 0; r < R; ++r) P[r][h] = c;
+        for (int r = 0; r < R; ++r) P[r][h] = c[h];
     }
     uint32_t om[R];
 #pragma unroll
@@ -229,10 +243,8 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
         const int4 rec = Ep[s];
-        const float2* rho = tp + (NT * QP + s * NT * QP) / 2;
         float2 rh[QH];
-#pragma unroll
-        for (int h = 0; h < QH; ++h) rh[h] = rho[h];
+        lds_pairs(rh, tp + NT * QP + s * NT * QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool o = one_fraction(xv[r][s], rec);
@@ -245,21 +257,18 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
       }
     }
     {
-      const float2* d = tp + QP / 2;
+      float2 d[QH];
+      lds_pairs(d, tp + QP);
 #pragma unroll
-      for (int h = 0; h < QH; ++h) {
-        const float2 dh = d[h];
+      for (int h = 0; h < QH; ++h)
 #pragma unroll
-        for (int r = 0; r < R; ++r) ph0[r] = __ffma2_rn(P[r][h], dh, ph0[r]);
-      }
+        for (int r = 0; r < R; ++r) ph0[r] = __ffma2_rn(P[r][h], d[h], ph0[r]);
     }
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        const float2* C = tp + (NT * QP + s * NT * QP + QP) / 2;
         float2 Ch[QH];
-#pragma unroll
-        for (int h = 0; h < QH; ++h) Ch[h] = C[h];
+        lds_pairs(Ch, tp + NT * QP + s * NT * QP + QP);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if ((om[r] >> s) & 1u) {
@@ -870,6 +879,7 @@ struct Args {
   void* out_phi;  // interaction kernel only: if set, the phi_i cells are also added to phi (fused call)
   int upper_only;  // interaction kernel only: write cells (i, j) with i < j only; mirror_kernel fills (j, i)
   int n_splits;
+  int tile_w;  // SHAP: row stride of the X / phi tiles = widest slot map + 1 (odd)
   int M, G;
   int64_t n_chunks;
   int max_chunk_bytes;
@@ -883,26 +893,54 @@ __host__ __device__ constexpr int tile_words_per_warp() {
   return R * 32 * ((S + 1) + (acc_width<kInter>(S) | 1));
 }
 
+// Row stride (words) of the X and phi tiles.  Interaction tiles are sized by
+// the slot width S (upper triangle of S x S); SHAP tiles by the blob's widest
+// slot map (tile_w = max slots + 1, odd: lanes = rows hit distinct banks), so
+// identity maps of M features cost M + 1 words per row, not S + 1.
+template <bool kInter, int S>
+__host__ __device__ constexpr int x_stride(int tile_w) { return kInter ? S + 1 : tile_w; }
+template <bool kInter, int S>
+__host__ __device__ constexpr int acc_stride(int tile_w) { return kInter ? (acc_width<kInter>(S) | 1) : tile_w; }
+
 // Launch shape per (dtype, kernel, slot width): R rows per lane and W warps
-// per block, chosen so that two blocks (tiles + chunk staging) share an SM.
+// per block.  Interactions and narrow SHAP tiles: two blocks (tiles + chunk
+// staging) share an SM.  Wide SHAP tiles (identity maps up to 64 features,
+// per-chunk maps of 32) trade warps for rows per lane: the per-path tables
+// are read from shared memory once per lane and used for R rows, which is
+// what bounds these kernels (LSU pipe, profiles/r01g).
+#ifndef GTS_SHAP_R32
+#define GTS_SHAP_R32 2
+#endif
+#ifndef GTS_SHAP_W32
+#define GTS_SHAP_W32 4
+#endif
+#ifndef GTS_SHAP_R64
+#define GTS_SHAP_R64 2
+#endif
+#ifndef GTS_SHAP_W64
+#define GTS_SHAP_W64 3
+#endif
 template <typename T, bool kInter, int S>
 struct Cfg {
+  static constexpr bool kWide = !kInter && S >= 32;
   static constexpr int R = (sizeof(T) == 4 && !kInter && S == 8) ? GTS_SHAP_R8
                            : (sizeof(T) == 4 && kInter && S == 8) ? GTS_INTER_R8
-                           : ((sizeof(T) == 4 && !kInter && S <= 16) ? 2
-                              : ((sizeof(T) == 4 && !kInter) ? GTS_SHAP_R_WIDE : 1));
+                           : (sizeof(T) == 4 && !kInter && S <= 16) ? 2
+                           : (sizeof(T) == 4 && kWide) ? (S == 32 ? GTS_SHAP_R32 : GTS_SHAP_R64)
+                                                       : 1;
   static constexpr int tile_bytes = (int)sizeof(T) * tile_words_per_warp<T, S, R, kInter>();
-  static constexpr int W = tile_bytes * 8 <= 74 * 1024   ? 8
+  static constexpr int W = (sizeof(T) == 4 && kWide) ? (S == 32 ? GTS_SHAP_W32 : GTS_SHAP_W64)
+                           : tile_bytes * 8 <= 74 * 1024  ? 8
                            : tile_bytes * 4 <= 80 * 1024  ? 4
                            : tile_bytes * 2 <= 160 * 1024 ? 2
                                                           : 1;  // 32-slot interaction tiles (528 pair cells per row)
-  static constexpr int kMinBlocks = 2;
 };
 
 // shared-memory layout: gauss (T) | X tiles (T) | phi tiles (T) | 2 staging buffers | 2 mbarriers
 template <typename T, int S, int W, int R, bool kInter>
-__host__ __device__ constexpr int staging_byte_offset() {
-  return (((kQMax * 3 * kQMax + W * tile_words_per_warp<T, S, R, kInter>()) * (int)sizeof(T)) + 127) & ~127;
+__host__ __device__ constexpr int staging_byte_offset(int tile_w) {
+  return (((kQMax * 3 * kQMax + W * R * 32 * (x_stride<kInter, S>(tile_w) + acc_stride<kInter, S>(tile_w))) *
+           (int)sizeof(T)) + 127) & ~127;
 }
 
 // ---- TMA bulk copy (global -> shared) completing on an mbarrier (PTX ISA:
@@ -937,13 +975,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 template <typename T, int S, int W, int R, bool kInter>
 __global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a) {
-  constexpr int XS = S + 1;
-  constexpr int AW = acc_width<kInter>(S);
-  constexpr int AS = AW | 1;
+  const int XS = x_stride<kInter, S>(a.tile_w);
+  const int AS = acc_stride<kInter, S>(a.tile_w);
+  const int AW = kInter ? acc_width<kInter>(S) : a.tile_w - 1;  // cells per row
   constexpr int ROWS = 32 * R;
   constexpr int o_x = kQMax * 3 * kQMax;
-  constexpr int o_acc = o_x + W * ROWS * XS;
-  constexpr int b_stage = staging_byte_offset<T, S, W, R, kInter>();
+  const int o_acc = o_x + W * ROWS * XS;
+  const int b_stage = staging_byte_offset<T, S, W, R, kInter>(a.tile_w);
   const int buf_bytes = a.max_chunk_bytes;  // multiple of 128 (host rounding)
   unsigned char* const stage0 = g_smem + b_stage;
   uint64_t* const bars = reinterpret_cast<uint64_t*>(stage0 + 2 * buf_bytes);

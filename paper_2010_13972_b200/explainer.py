@@ -6,6 +6,8 @@ once per model and is amortised over all rows.
 """
 from __future__ import annotations
 
+import time
+
 import numpy as np
 import torch
 
@@ -36,22 +38,50 @@ class Blob:
         dev = host.to(device, non_blocking=True) if device is not None else host
         return cls(info, dev)
 
+    _seq = 0  # broadcasts issued by this process (same order on every rank)
+
     def broadcast(self, src: int = 0, group=None) -> "Blob":
-        """Replicate this rank's blob to all ranks: ONE broadcast of the bytes
-        (NCCL over NVLink on GPUs), preceded by the small info record."""
+        """Replicate the source rank's blob to every rank with ONE collective:
+        a broadcast of the blob bytes (NCCL over NVLink on GPUs).  The 256-byte
+        info record, which the receivers need to size their buffer, goes
+        through the process group's rendezvous store (host key-value plumbing,
+        no device collective).  Returns self (receivers' data/info replaced)."""
         import torch.distributed as dist
-        dev = self.data.device
-        meta = torch.zeros(256, dtype=torch.uint8, device=dev)
-        if dist.get_rank(group) == src:
-            raw = np.frombuffer(self.info.to_bytes(), np.uint8)
-            meta[:len(raw)] = torch.from_numpy(raw.copy()).to(dev)
-        dist.broadcast(meta, src, group=group)
-        info = gts.gts_blob_info.from_bytes(meta.cpu().numpy().tobytes())
-        if dist.get_rank(group) != src:
-            self.data = torch.empty(info.bytes, dtype=torch.uint8, device=dev)
+        rank = dist.get_rank(group)
+        Blob._seq += 1
+        key = f"gts_blob_info/{Blob._seq}"
+        store = _default_store()
+        if store is not None:
+            if rank == src:
+                store.set(key, self.info.to_bytes())
+            else:
+                self.info = gts.gts_blob_info.from_bytes(store.get(key))
+        else:  # no store reachable: the info record travels as a second, 256-byte broadcast
+            dev = self.data.device
+            meta = torch.zeros(256, dtype=torch.uint8, device=dev)
+            if rank == src:
+                raw = np.frombuffer(self.info.to_bytes(), np.uint8)
+                meta[:len(raw)] = torch.from_numpy(raw.copy()).to(dev)
+            dist.broadcast(meta, src, group=group)
+            self.info = gts.gts_blob_info.from_bytes(meta.cpu().numpy().tobytes())
+        if rank != src:
+            self.data = torch.empty(self.info.bytes, dtype=torch.uint8, device=self.data.device)
         dist.broadcast(self.data, src, group=group)
-        self.info = info
         return self
+
+
+def row_shard(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [floor(r n / N), floor((r+1) n / N)) of rank r; rows
+    are independent, so no collective touches them."""
+    return n_total * rank // world, n_total * (rank + 1) // world
+
+
+def _default_store():
+    try:
+        from torch.distributed import distributed_c10d as c10d
+        return c10d._get_default_store()
+    except Exception:
+        return None
 
 
 class TreeShapExplainer:
@@ -64,12 +94,14 @@ class TreeShapExplainer:
 
     def __init__(self, model, dtype: str = "f32", pack: str = "bfd", layout: str = "nodal",
                  device=None, max_slots: int = 0, interactions: bool = True, build_blobs: bool = True,
-                 inter_max_slots: int = 0, validate: bool = False):
+                 inter_max_slots: int = 0, validate: bool = False, host_tables: bool = True):
         """interactions: build the interaction blob now (True) or on the first
         interaction call (False); it is never a reason to fail.  build_blobs=False
         defers both blobs (multi-GPU ranks that receive them by broadcast).
         validate: check every X for NaN / inf first (gts_validate_x, reading
-        G17; costs a pass over X and a stream synchronisation)."""
+        G17; costs a pass over X and a stream synchronisation).
+        host_tables=False skips extraction and packing too (a rank that only
+        receives blobs, see replicated())."""
         self.validate = bool(validate)
         self.dtype_code, self.torch_dtype, self.np_dtype = _DT[dtype]
         self.layout = gts.LAYOUTS[layout] if isinstance(layout, str) else int(layout)
@@ -79,20 +111,70 @@ class TreeShapExplainer:
         self.n_groups = int(model.n_groups)
         self.max_slots = int(max_slots)
         self.inter_max_slots = int(inter_max_slots)
-        self.paths = gts.gts_extract_paths(model)
-        self.bins = gts.gts_binpack(self.paths, 32, pack)
+        self.timings = {}
+        self.paths = self.bins = None
         self._blob = self._blob_int = None
+        if not host_tables:
+            return
+        t0 = time.perf_counter()
+        self.paths = gts.gts_extract_paths(model)
+        t1 = time.perf_counter()
+        self.bins = gts.gts_binpack(self.paths, 32, pack)
+        self.timings.update(extract_s=t1 - t0, pack_s=time.perf_counter() - t1)
         if build_blobs:
             self._blob = self._make_blob(False)
             if interactions:
                 _ = self.blob_int
 
     def _make_blob(self, for_interactions: bool) -> Blob:
+        if self.bins is None:
+            raise RuntimeError("this explainer has no host tables (host_tables=False): its blobs arrive by broadcast")
+        t0 = time.perf_counter()
         if self.layout == gts.GTS_LAYOUT_NODAL and for_interactions:
             info = gts.gts_blob_plan_for(self.bins, self.dtype_code, self.layout, self.inter_max_slots,
                                          "interactions")
-            return Blob.from_info(self.bins, info, self.device)
-        return Blob.from_bins(self.bins, self.dtype_code, self.layout, self.max_slots, self.device)
+        else:
+            info = gts.gts_blob_plan(self.bins, self.dtype_code, self.layout, self.max_slots)
+        t1 = time.perf_counter()
+        b = Blob.from_info(self.bins, info, self.device)
+        if self.device is not None and self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
+        k = "int_" if for_interactions else ""
+        self.timings[k + "plan_s"] = t1 - t0
+        self.timings[k + "write_h2d_s"] = time.perf_counter() - t1
+        return b
+
+    @classmethod
+    def replicated(cls, model, mode: str = "shap", src: int = 0, group=None, **kw) -> "TreeShapExplainer":
+        """Multi-GPU setup: rank `src` alone
+        extracts, packs and writes the one blob `mode` needs ("shap": the SHAP
+        blob; "interactions" / "both": the interaction blob, which the fused
+        call also reads phi from), and ONE broadcast replicates it
+        (Blob.broadcast); the other ranks do no host-side method work.  Rows
+        are then sharded by the caller, with no further collectives."""
+        import torch.distributed as dist
+        rank = dist.get_rank(group)
+        want_int = mode in ("interactions", "both")
+        if rank == src:
+            ex = cls(model, interactions=False, build_blobs=False, **kw)
+            blob = ex.blob_int if want_int else ex.blob
+        else:
+            ex = cls(model, interactions=False, host_tables=False, **kw)
+            blob = Blob(None, torch.empty(0, dtype=torch.uint8, device=ex.device))
+        t0 = time.perf_counter()
+        blob.broadcast(src, group)
+        if ex.device is not None and ex.device.type == "cuda":
+            torch.cuda.synchronize(ex.device)
+        ex.timings["broadcast_s"] = time.perf_counter() - t0
+        if want_int:
+            ex._blob_int = blob
+            if blob.info.uses & gts.GTS_USE_SHAP:
+                ex._blob = blob
+        else:
+            ex._blob = blob
+            if blob.info.uses & gts.GTS_USE_INTERACTIONS:
+                ex._blob_int = blob
+        return ex
 
     @property
     def blob(self) -> Blob:

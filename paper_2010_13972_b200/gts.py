@@ -61,7 +61,8 @@ class gts_blob_info(ctypes.Structure):
                 ("shap_flops_per_row", _dbl), ("inter_flops_per_row", _dbl),
                 ("paper_shap_flops_per_row", _dbl), ("paper_inter_flops_per_row", _dbl),
                 ("max_chunk_bytes", _i64), ("max_chunk_elems", _i64), ("max_chunk_paths", _i64),
-                ("uses", _i32), ("n_tables", _i32), ("reserved", _i64 * 4)]
+                ("uses", _i32), ("n_tables", _i32), ("max_chunk_slots", _i32), ("chunk_bytes", _i32),
+                ("reserved", _i64 * 3)]
 
     def to_bytes(self) -> bytes:
         return ctypes.string_at(ctypes.addressof(self), ctypes.sizeof(self))
