@@ -59,6 +59,10 @@ namespace nodal {
 
 extern __shared__ __align__(16) unsigned char g_smem[];
 
+#ifndef GTS_RMW_REGS
+#define GTS_RMW_REGS 8  // registers per lane for grouped tile read-modify-writes (R rows x cells)
+#endif
+
 template <int Q>
 struct QP_ {
   static constexpr int v = (Q + 3) & ~3;
@@ -118,6 +122,7 @@ template <typename T, int Q, int R, int NT>
 __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restrict__ E, const T* __restrict__ tab,
                                          const int (&xb)[R], const int (&ab)[R]) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q;
+  constexpr int kRmw = GTS_RMW_REGS / R > 1 ? GTS_RMW_REGS / R : 1;
   T* const sT = reinterpret_cast<T*>(g_smem);
   const int words = nodal_path_words(k, Q, NT);
   int slot[KM];
@@ -191,11 +196,28 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
       }
     }
   }
+  // The run's slots are distinct features (merged paths), so the tile cells are
+  // updated in groups of kRmw: kRmw loads, then kRmw stores, instead of each
+  // read-modify-write waiting for the previous store (the compiler cannot
+  // prove runtime slots distinct, so it keeps them in program order).
 #pragma unroll
-  for (int s = 0; s < KM; ++s)
-    if (s < KM - 1 || s < k)
+  for (int s0 = 0; s0 < KM; s0 += kRmw) {
+    T old[R][kRmw];
 #pragma unroll
-      for (int r = 0; r < R; ++r) sT[ab[r] + slot[s]] += acc[r][s] + ph0[r];
+    for (int b = 0; b < kRmw; ++b) {
+      const int s = s0 + b;
+      if (s < KM && (s < KM - 1 || s < k))
+#pragma unroll
+        for (int r = 0; r < R; ++r) old[r][b] = sT[ab[r] + slot[s]];
+    }
+#pragma unroll
+    for (int b = 0; b < kRmw; ++b) {
+      const int s = s0 + b;
+      if (s < KM && (s < KM - 1 || s < k))
+#pragma unroll
+        for (int r = 0; r < R; ++r) sT[ab[r] + slot[s]] = old[r][b] + (acc[r][s] + ph0[r]);
+    }
+  }
 }
 
 // fp32 variant of shap_run on packed pairs of Gauss nodes: {P_q, P_q+1} live
@@ -208,6 +230,7 @@ template <int Q, int R, int NT>
 __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __restrict__ E,
                                             const float* __restrict__ tab, const int (&xb)[R], const int (&ab)[R]) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q, QH = (Q + 1) / 2;
+  constexpr int kRmw = GTS_RMW_REGS / R > 1 ? GTS_RMW_REGS / R : 1;
   float* const sT = reinterpret_cast<float*>(g_smem);
   const int words = nodal_path_words(k, Q, NT);
   int slot[KM];
@@ -280,10 +303,24 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
     }
   }
 #pragma unroll
-  for (int s = 0; s < KM; ++s)
-    if (s < KM - 1 || s < k)
+  for (int s0 = 0; s0 < KM; s0 += kRmw) {  // grouped read-modify-writes, see shap_run
+    float old[R][kRmw];
 #pragma unroll
-      for (int r = 0; r < R; ++r) sT[ab[r] + slot[s]] += (acc[r][s].x + acc[r][s].y) + (ph0[r].x + ph0[r].y);
+    for (int b = 0; b < kRmw; ++b) {
+      const int s = s0 + b;
+      if (s < KM && (s < KM - 1 || s < k))
+#pragma unroll
+        for (int r = 0; r < R; ++r) old[r][b] = sT[ab[r] + slot[s]];
+    }
+#pragma unroll
+    for (int b = 0; b < kRmw; ++b) {
+      const int s = s0 + b;
+      if (s < KM && (s < KM - 1 || s < k))
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          sT[ab[r] + slot[s]] = old[r][b] + ((acc[r][s].x + acc[r][s].y) + (ph0[r].x + ph0[r].y));
+    }
+  }
 }
 
 // One path, element loop not unrolled (large Q); accumulates per element.
@@ -909,16 +946,22 @@ __host__ __device__ constexpr int acc_stride(int tile_w) { return kInter ? (acc_
 // are read from shared memory once per lane and used for R rows, which is
 // what bounds these kernels (LSU pipe, profiles/r01g).
 #ifndef GTS_SHAP_R32
-#define GTS_SHAP_R32 2
+#define GTS_SHAP_R32 1  // measured (profiles/r02b): R 1 / W 8 3.02e5 rows/s fashion, R 2 / W 4 2.49e5
 #endif
 #ifndef GTS_SHAP_W32
-#define GTS_SHAP_W32 4
+#define GTS_SHAP_W32 8
+#endif
+#ifndef GTS_SHAP_B32
+#define GTS_SHAP_B32 2  // resident blocks per SM the register budget is sized for
 #endif
 #ifndef GTS_SHAP_R64
-#define GTS_SHAP_R64 2
+#define GTS_SHAP_R64 1
 #endif
 #ifndef GTS_SHAP_W64
-#define GTS_SHAP_W64 3
+#define GTS_SHAP_W64 6
+#endif
+#ifndef GTS_SHAP_B64
+#define GTS_SHAP_B64 2
 #endif
 template <typename T, bool kInter, int S>
 struct Cfg {
@@ -934,6 +977,8 @@ struct Cfg {
                            : tile_bytes * 4 <= 80 * 1024  ? 4
                            : tile_bytes * 2 <= 160 * 1024 ? 2
                                                           : 1;  // 32-slot interaction tiles (528 pair cells per row)
+  static constexpr int kMinBlocks = (sizeof(T) == 4 && kWide) ? (S == 32 ? GTS_SHAP_B32 : GTS_SHAP_B64)
+                                                              : (W >= 8 ? 2 : 1);
 };
 
 // shared-memory layout: gauss (T) | X tiles (T) | phi tiles (T) | 2 staging buffers | 2 mbarriers
@@ -974,7 +1019,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 template <typename T, int S, int W, int R, bool kInter>
-__global__ void __launch_bounds__(W * 32, (W >= 8 ? 2 : 1)) nodal_kernel(Args a) {
+__global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal_kernel(Args a) {
   const int XS = x_stride<kInter, S>(a.tile_w);
   const int AS = acc_stride<kInter, S>(a.tile_w);
   const int AW = kInter ? acc_width<kInter>(S) : a.tile_w - 1;  // cells per row

@@ -1,20 +1,21 @@
 #!/bin/bash
-# Kernel-shape variants of the wide SHAP kernels (covtype-large S=64 identity,
-# fashion_mnist-med S=32 slot maps) on one B200: bench lines per variant lib.
-out=${1:-gpurun_out/r02_var}
+# Kernel-shape variants (built with _build.build(out=..., defines=...)) on one
+# B200: one short bench line per (variant lib, workload).
+out=${1:-gpurun_out/r02_var}; shift
+vars=${@:-main}
 mkdir -p $out
 Q="--steps 3 --warmup 1 --no-e2e --no-ablation --no-cpu-baseline --extras none"
-for v in default c8 w6 r1w8; do
+for v in $vars; do
   lib=paper_2010_13972_b200/_lib/libgts.so
-  [ $v != default ] && lib=paper_2010_13972_b200/_lib/var_$v.so
+  [ $v != main ] && lib=paper_2010_13972_b200/_lib/var_$v.so
   [ -f $lib ] || continue
   GTS_LIB=$lib timeout 600 python bench.py --workload covtype-large --mode shap --rows-per-step 65536 $Q > $out/covtype_$v.json 2> $out/covtype_$v.err
-  GTS_LIB=$lib timeout 600 python bench.py --workload fashion_mnist-med --mode shap --rows-per-gpu 65536 --rows-per-step 65536 $Q > $out/fashion_$v.json 2> $out/fashion_$v.err
+  case $v in main|rmw1)
+    GTS_LIB=$lib timeout 600 python bench.py --workload fashion_mnist-med --mode shap --rows-per-gpu 65536 --rows-per-step 65536 $Q > $out/fashion_$v.json 2> $out/fashion_$v.err
+    GTS_LIB=$lib timeout 600 python bench.py --workload cal_housing-med --mode shap --rows-per-step 0 $Q > $out/calmed_shap_$v.json 2> $out/calmed_shap_$v.err
+    GTS_LIB=$lib timeout 600 python bench.py --workload adult-large --mode shap --rows-per-gpu 65536 --rows-per-step 0 $Q > $out/adult_shap_$v.json 2> $out/adult_shap_$v.err;;
+  esac
 done
-GTS_LIB=paper_2010_13972_b200/_lib/libgts.so timeout 600 python bench.py --workload fashion_mnist-med --mode shap --max-slots 64 --rows-per-gpu 65536 --rows-per-step 65536 $Q > $out/fashion_s64.json 2> $out/fashion_s64.err
-timeout 600 python bench.py --workload cal_housing-med --mode both --rows-per-step 0 $Q > $out/calmed_both.json 2> $out/calmed_both.err
-timeout 600 python bench.py --workload cal_housing-med --mode shap --rows-per-step 0 $Q > $out/calmed_shap.json 2> $out/calmed_shap.err
-timeout 900 python bench.py --workload adult-large --mode both --rows-per-gpu 65536 --rows-per-step 0 $Q > $out/adult_both.json 2> $out/adult_both.err
 for f in $out/*.json; do python - "$f" <<'PY'
 import json,sys
 try:
