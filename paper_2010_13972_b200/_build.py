@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libgts.so")
 SOURCES = [os.path.join(CSRC, "host.cpp"), os.path.join(CSRC, "kernels.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("blob_format.h", "nodal.cuh", "warp_bins.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("blob_format.h", "nodal.cuh", "warp_bins.cuh", "trace.h")] + [
     os.path.join(ROOT, "include", "gts.h")]
 
 NVCC_FLAGS = [

@@ -21,6 +21,7 @@
 
 #include "../../include/gts.h"
 #include "blob_format.h"
+#include "trace.h"
 
 namespace gts {
 
@@ -337,25 +338,69 @@ static int64_t pack_ffd(const std::vector<int32_t>& size, int32_t cap, std::vect
   return n_bins;
 }
 
-// BFD with an ordered set of (residual, bin) ("implemented easily
-// using std::set"); lower_bound gives the smallest residual >= s, lowest bin id.
+// Set of bin ids with lowest-member lookup: a three-level 64-ary bitset
+// (level 2 scanned from a cursor below which it is known to be empty).
+class IdBitset {
+ public:
+  explicit IdBitset(int64_t n)
+      : l0_((n + 63) / 64, 0), l1_((l0_.size() + 63) / 64, 0), l2_((l1_.size() + 63) / 64, 0) {}
+  bool empty() const { return count_ == 0; }
+  void insert(int64_t b) {
+    ++count_;
+    l0_[b >> 6] |= 1ull << (b & 63);
+    l1_[b >> 12] |= 1ull << ((b >> 6) & 63);
+    l2_[b >> 18] |= 1ull << ((b >> 12) & 63);
+    if ((b >> 18) < lo_) lo_ = b >> 18;
+  }
+  void erase(int64_t b) {
+    --count_;
+    if ((l0_[b >> 6] &= ~(1ull << (b & 63))) != 0) return;
+    if ((l1_[b >> 12] &= ~(1ull << ((b >> 6) & 63))) != 0) return;
+    l2_[b >> 18] &= ~(1ull << ((b >> 12) & 63));
+  }
+  int64_t lowest() {  // precondition: !empty()
+    while (l2_[lo_] == 0) ++lo_;
+    const int64_t w2 = lo_, w1 = (w2 << 6) + __builtin_ctzll(l2_[w2]);
+    const int64_t w0 = (w1 << 6) + __builtin_ctzll(l1_[w1]);
+    return (w0 << 6) + __builtin_ctzll(l0_[w0]);
+  }
+
+ private:
+  std::vector<uint64_t> l0_, l1_, l2_;
+  int64_t lo_ = 0, count_ = 0;
+};
+
+// BFD: the open bin with the smallest residual >= s, ties to the
+// lowest bin id.  Residuals are 1..cap (<= 32), so the open bins are kept in one
+// id set per residual plus a bit mask of the non-empty residuals: the best bin
+// is the lowest id of residual ctz(mask >> s) + s.  (The paper's std::set of
+// (residual, bin) pairs gives the same packing, 5-10x slower at 6.6M items.)
 static int64_t pack_bfd(const std::vector<int32_t>& size, int32_t cap, std::vector<int32_t>& bin_of) {
-  std::set<std::pair<int32_t, int64_t>> open;
+  const int64_t n = (int64_t)size.size();
+  std::vector<IdBitset> open;
+  open.reserve(cap + 1);
+  for (int32_t r = 0; r <= cap; ++r) open.emplace_back(std::max<int64_t>(n, 1));
+  uint64_t nonempty = 0;  // bit r: some open bin has residual r
   int64_t n_bins = 0;
   for (int64_t i : decreasing_order(size, cap)) {
     const int32_t s = size[i];
-    auto it = open.lower_bound({s, (int64_t)-1});
+    const uint64_t fit = nonempty >> s;
     int64_t b;
     int32_t res;
-    if (it == open.end()) {
+    if (fit == 0) {
       b = n_bins++;
       res = cap - s;
     } else {
-      b = it->second;
-      res = it->first - s;
-      open.erase(it);
+      const int32_t r = s + __builtin_ctzll(fit);
+      b = open[r].lowest();
+      open[r].erase(b);
+      if (open[r].empty()) nonempty &= ~(1ull << r);
+      res = r - s;
     }
-    if (res > 0) open.insert({res, b});
+    if (res > 0) {
+      open[res].insert(b);
+      nonempty |= 1ull << res;
+    }
     bin_of[i] = (int32_t)b;
   }
   return n_bins;
@@ -534,123 +579,179 @@ static void plan_nodal(const PathTable& tab, int S, int nt, size_t tsize, NodalP
       if (tab.feature[tab.path_offset[a] + i] != tab.feature[tab.path_offset[b] + i]) return false;
     return true;
   };
-  std::vector<std::vector<int64_t>> by_group(tab.n_groups);
+  const int32_t G = tab.n_groups;
+  std::vector<std::vector<int64_t>> by_group(G);
   for (int64_t p = 0; p < L; ++p)
     if (tab.len(p) > 1) by_group[tab.group[p]].push_back(p);
-  if (identity) {
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int32_t g = 0; g < tab.n_groups; ++g) std::sort(by_group[g].begin(), by_group[g].end(), fs_less);
-  }
-  std::vector<int64_t> order;
-  order.reserve(L);
-  for (auto& v : by_group) {
-    order.insert(order.end(), v.begin(), v.end());
-    std::vector<int64_t>().swap(v);
-  }
   // (Cutting small models into ~one chunk per SM lowered the 1-row latency of
   // cal_housing-small from 23 to 18 us but cost 30 % at 2^20 rows, since runs
   // and staging get shorter; profiles/r01h.  Not adopted.)
-  const int chunk_paths = kMaxChunkPaths;
   // staged bytes of a chunk: element records + path headers (16 B each) + tables
   auto path_bytes = [&](int k, int q) { return (int64_t)16 * (k + 1) + (int64_t)tsize * nodal_path_words(k, q, nt); };
-  int32_t map_id = -1;
-  int32_t cur_map[64];
-  int n_cur = 0;
-  int32_t feats[64], u[128];
-  std::vector<int64_t> members;
-  size_t i = 0;
-  while (i < order.size()) {
-    ChunkRec c{};
-    c.group = tab.group[order[i]];
-    c.path_begin = (int64_t)np.paths.size();
-    c.elem_begin = (int64_t)np.slots.size();
+
+  // Chunks never span groups, so every group is planned on its own (in
+  // parallel) with group-local offsets; the pieces are then concatenated in
+  // group order, which gives the same plan as one pass over all groups.
+  struct Part {
+    std::vector<ChunkRec> chunks;    // path_begin / elem_begin local; slotmap_begin local to `maps`
+    std::vector<int32_t> maps;       // this group's slot maps (one per local map id)
+    std::vector<PathRec> paths;
+    std::vector<uint8_t> slots;
+    std::vector<double> ws, wi;
+  };
+  std::vector<Part> parts(G);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int32_t g = 0; g < G; ++g) {
+    std::vector<int64_t>& order = by_group[g];
+    if (identity) std::sort(order.begin(), order.end(), fs_less);
+    Part& pt = parts[g];
+    int32_t map_id = -1, n_cur = 0;
+    int32_t cur_map[64], feats[64], u[128];
     int nf = 0;
-    members.clear();
-    int64_t bytes = 0, nel = 0;
-    size_t j = i;
-    while (j < order.size() && (int)members.size() < chunk_paths) {
-      const int64_t p = order[j];
-      if (tab.group[p] != c.group) break;
-      const int k = tab.len(p) - 1, q = (k + 1) / 2;
-      const int64_t w = path_bytes(k, q);
-      if (!members.empty() && bytes + w > chunk_bytes) break;
-      if (!identity) {  // union of two sorted feature lists
-        const int32_t* pf = &tab.feature[tab.path_offset[p] + 1];
-        int a = 0, b = 0, n = 0;
-        while (a < nf || b < k) {
-          int32_t x;
-          if (b >= k || (a < nf && feats[a] < pf[b])) x = feats[a++];
-          else if (a >= nf || pf[b] < feats[a]) x = pf[b++];
-          else { x = feats[a++]; ++b; }
-          u[n++] = x;
+    std::vector<int64_t> members;
+    size_t i = 0;
+    while (i < order.size()) {
+      ChunkRec c{};
+      c.group = g;
+      c.path_begin = (int64_t)pt.paths.size();
+      c.elem_begin = (int64_t)pt.slots.size();
+      nf = 0;
+      members.clear();
+      int64_t bytes = 0, nel = 0;
+      size_t j = i;
+      while (j < order.size() && (int)members.size() < kMaxChunkPaths) {
+        const int64_t p = order[j];
+        const int k = tab.len(p) - 1, q = (k + 1) / 2;
+        const int64_t w = path_bytes(k, q);
+        if (!members.empty() && bytes + w > chunk_bytes) break;
+        if (!identity) {  // union of two sorted feature lists
+          const int32_t* pf = &tab.feature[tab.path_offset[p] + 1];
+          int a = 0, b = 0, n = 0;
+          while (a < nf || b < k) {
+            int32_t x;
+            if (b >= k || (a < nf && feats[a] < pf[b])) x = feats[a++];
+            else if (a >= nf || pf[b] < feats[a]) x = pf[b++];
+            else { x = feats[a++]; ++b; }
+            u[n++] = x;
+          }
+          if (!members.empty() && n > S) break;
+          std::memcpy(feats, u, sizeof(int32_t) * n);
+          nf = n;
         }
-        if (!members.empty() && n > S) break;
-        std::memcpy(feats, u, sizeof(int32_t) * n);
-        nf = n;
+        members.push_back(p);
+        bytes += w;
+        nel += k;
+        ++j;
       }
-      members.push_back(p);
-      bytes += w;
-      nel += k;
-      ++j;
-    }
-    if (identity) {
-      nf = M;
-      for (int32_t f = 0; f < M; ++f) feats[f] = f;
-    }
-    // inside the chunk: Q descending (template locality), then feature set (runs)
-    std::sort(members.begin(), members.end(), fs_less);
-    if (map_id < 0 || nf != n_cur || std::memcmp(feats, cur_map, sizeof(int32_t) * nf) != 0) {
-      ++map_id;
-      n_cur = nf;
-      std::memcpy(cur_map, feats, sizeof(int32_t) * nf);
-      c.slotmap_begin = (int64_t)np.slotmap.size();
-      np.slotmap.insert(np.slotmap.end(), feats, feats + nf);
-    } else {
-      c.slotmap_begin = np.chunks.back().slotmap_begin;
-    }
-    c.map_id = map_id;
-    c.n_slots = (int32_t)nf;
-    c.n_paths = (int32_t)members.size();
-    c.n_elems = (int32_t)nel;
-    int32_t table = 0, rel = 0, maxq = 0;
-    double ws = 0, wi = 0;
-    size_t run_head = 0;
-    for (size_t mi = 0; mi < members.size(); ++mi) {
-      const int64_t p = members[mi];
-      const int k = tab.len(p) - 1, q = (k + 1) / 2;
-      if (mi == 0 || !same_set(members[run_head], p)) run_head = mi;
-      const size_t head_index = np.paths.size() - (mi - run_head);
-      PathRec pr{};
-      pr.k = k;
-      if (run_head == mi) pr.k |= 1 << 16;
-      else np.paths[head_index].k += 1 << 16;
-      pr.q = q;
-      pr.elem = rel;
-      pr.table = table;
-      pr.src = p;
-      np.paths.push_back(pr);
-      for (int64_t e = tab.path_offset[p] + 1; e < tab.path_offset[p + 1]; ++e) {
-        const int32_t f = tab.feature[e];
-        np.slots.push_back((uint8_t)(identity ? f : (std::lower_bound(feats, feats + nf, f) - feats)));
+      if (identity) {
+        nf = M;
+        for (int32_t f = 0; f < M; ++f) feats[f] = f;
       }
-      rel += k;
-      table += nodal_path_words(k, q, nt);
-      maxq = std::max(maxq, q);
-      ws += nodal_shap_flops(k, q);
-      wi += nodal_inter_flops(k, q);
+      // inside the chunk: Q descending (template locality), then feature set (runs)
+      std::sort(members.begin(), members.end(), fs_less);
+      if (map_id < 0 || nf != n_cur || std::memcmp(feats, cur_map, sizeof(int32_t) * nf) != 0) {
+        ++map_id;
+        n_cur = nf;
+        std::memcpy(cur_map, feats, sizeof(int32_t) * nf);
+        c.slotmap_begin = (int64_t)pt.maps.size();
+        pt.maps.insert(pt.maps.end(), feats, feats + nf);
+      } else {
+        c.slotmap_begin = pt.chunks.back().slotmap_begin;
+      }
+      c.map_id = map_id;
+      c.n_slots = (int32_t)nf;
+      c.n_paths = (int32_t)members.size();
+      c.n_elems = (int32_t)nel;
+      int32_t table = 0, rel = 0, maxq = 0;
+      double ws = 0, wi = 0;
+      size_t run_head = 0;
+      for (size_t mi = 0; mi < members.size(); ++mi) {
+        const int64_t p = members[mi];
+        const int k = tab.len(p) - 1, q = (k + 1) / 2;
+        if (mi == 0 || !same_set(members[run_head], p)) run_head = mi;
+        const size_t head_index = pt.paths.size() - (mi - run_head);
+        PathRec pr{};
+        pr.k = k;
+        if (run_head == mi) pr.k |= 1 << 16;
+        else pt.paths[head_index].k += 1 << 16;
+        pr.q = q;
+        pr.elem = rel;
+        pr.table = table;
+        pr.src = p;
+        pt.paths.push_back(pr);
+        for (int64_t e = tab.path_offset[p] + 1; e < tab.path_offset[p + 1]; ++e) {
+          const int32_t f = tab.feature[e];
+          pt.slots.push_back((uint8_t)(identity ? f : (std::lower_bound(feats, feats + nf, f) - feats)));
+        }
+        rel += k;
+        table += nodal_path_words(k, q, nt);
+        maxq = std::max(maxq, q);
+        ws += nodal_shap_flops(k, q);
+        wi += nodal_inter_flops(k, q);
+      }
+      c.table_words = table;
+      c.max_q = maxq;
+      c.data_bytes = (int32_t)(16 * ((int64_t)nel + c.n_paths) + (int64_t)tsize * table);
+      c.data_bytes = (c.data_bytes + 15) & ~15;
+      pt.chunks.push_back(c);
+      pt.ws.push_back(ws);
+      pt.wi.push_back(wi);
+      i = j;
     }
-    c.table_words = table;
-    c.max_q = maxq;
-    c.data_bytes = (int32_t)(16 * ((int64_t)nel + c.n_paths) + (int64_t)tsize * table);
-    c.data_bytes = (c.data_bytes + 15) & ~15;
-    np.max_words = std::max<int64_t>(np.max_words, c.data_bytes);
-    np.max_elems = std::max<int64_t>(np.max_elems, nel);
-    np.max_paths = std::max<int64_t>(np.max_paths, c.n_paths);
-    np.max_slots_used = std::max<int32_t>(np.max_slots_used, c.n_slots);
-    np.chunks.push_back(c);
-    np.work_shap.push_back(ws);
-    np.work_inter.push_back(wi);
-    i = j;
+    std::vector<int64_t>().swap(order);
+  }
+  // concatenate: global offsets, and map ids that (as in one pass) continue
+  // the previous chunk's id when its slot map is identical
+  size_t n_chunks = 0, n_paths = 0, n_slots = 0;
+  for (const Part& pt : parts) {
+    n_chunks += pt.chunks.size();
+    n_paths += pt.paths.size();
+    n_slots += pt.slots.size();
+  }
+  np.chunks.reserve(n_chunks);
+  np.work_shap.reserve(n_chunks);
+  np.work_inter.reserve(n_chunks);
+  np.paths.reserve(n_paths);
+  np.slots.reserve(n_slots);
+  int32_t gmap = -1;
+  const int32_t* gmap_ptr = nullptr;
+  int32_t gmap_n = 0;
+  for (Part& pt : parts) {
+    const int64_t path0 = (int64_t)np.paths.size(), elem0 = (int64_t)np.slots.size();
+    int32_t last_local = -1;
+    for (size_t ci = 0; ci < pt.chunks.size(); ++ci) {
+      ChunkRec c = pt.chunks[ci];
+      c.path_begin += path0;
+      c.elem_begin += elem0;
+      if (c.map_id != last_local) {
+        last_local = c.map_id;
+        const int32_t* mp = pt.maps.data() + c.slotmap_begin;
+        if (gmap < 0 || c.n_slots != gmap_n || std::memcmp(mp, gmap_ptr, sizeof(int32_t) * c.n_slots) != 0) {
+          ++gmap;
+          gmap_n = c.n_slots;
+          c.slotmap_begin = (int64_t)np.slotmap.size();
+          np.slotmap.insert(np.slotmap.end(), mp, mp + c.n_slots);
+        } else {
+          c.slotmap_begin = np.chunks.back().slotmap_begin;
+        }
+        gmap_ptr = np.slotmap.data() + c.slotmap_begin;
+      } else {
+        c.slotmap_begin = np.chunks.back().slotmap_begin;
+      }
+      c.map_id = gmap;
+      np.max_words = std::max<int64_t>(np.max_words, c.data_bytes);
+      np.max_elems = std::max<int64_t>(np.max_elems, c.n_elems);
+      np.max_paths = std::max<int64_t>(np.max_paths, c.n_paths);
+      np.max_slots_used = std::max<int32_t>(np.max_slots_used, c.n_slots);
+      np.chunks.push_back(c);
+    }
+    np.work_shap.insert(np.work_shap.end(), pt.ws.begin(), pt.ws.end());
+    np.work_inter.insert(np.work_inter.end(), pt.wi.begin(), pt.wi.end());
+    np.paths.insert(np.paths.end(), pt.paths.begin(), pt.paths.end());
+    np.slots.insert(np.slots.end(), pt.slots.begin(), pt.slots.end());
+    Part().chunks.swap(pt.chunks);
+    std::vector<PathRec>().swap(pt.paths);
+    std::vector<uint8_t>().swap(pt.slots);
   }
 }
 
@@ -1025,6 +1126,7 @@ extern "C" {
 
 gts_status gts_extract_paths(const gts_model* model, gts_paths** out) {
   if (!out) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "out is NULL");
+  GTS_NVTX("gts_extract_paths");
   try {
     std::shared_ptr<gts::PathTable> tab;
     gts_status st = gts::extract(model, tab);
@@ -1060,6 +1162,7 @@ void gts_paths_free(gts_paths* paths) { delete paths; }
 
 gts_status gts_binpack(const gts_paths* paths, int32_t capacity, gts_pack_algo algo, gts_bins** out) {
   if (!paths || !out) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
+  GTS_NVTX("gts_binpack");
   try {
     auto b = std::make_unique<gts_bins>();
     gts_status st = gts::binpack(paths->tab, capacity, (int32_t)algo, *b);
@@ -1089,6 +1192,7 @@ void gts_bins_free(gts_bins* b) { delete b; }
 
 gts_status gts_blob_plan(const gts_bins* bins, gts_dtype dtype, gts_layout layout, int32_t max_slots,
                          gts_blob_info* info) {
+  GTS_NVTX("gts_blob_plan");
   try {
     return gts::blob_plan_cached(bins, (int32_t)dtype, (int32_t)layout, max_slots, 0, info);
   } catch (const std::bad_alloc&) {
@@ -1100,6 +1204,7 @@ gts_status gts_blob_plan_for(const gts_bins* bins, gts_dtype dtype, gts_layout l
                              gts_blob_use uses, gts_blob_info* info) {
   if ((int32_t)uses < GTS_USE_SHAP || (int32_t)uses > GTS_USE_BOTH)
     return gts::fail(GTS_ERR_INVALID_ARGUMENT, "bad blob uses %d", (int)uses);
+  GTS_NVTX("gts_blob_plan_for");
   try {
     return gts::blob_plan_cached(bins, (int32_t)dtype, (int32_t)layout, max_slots, (int32_t)uses, info);
   } catch (const std::bad_alloc&) {
@@ -1108,6 +1213,7 @@ gts_status gts_blob_plan_for(const gts_bins* bins, gts_dtype dtype, gts_layout l
 }
 
 gts_status gts_blob_write(const gts_bins* bins, const gts_blob_info* info, void* host_dst, size_t dst_bytes) {
+  GTS_NVTX("gts_blob_write");
   try {
     return gts::blob_write(bins, info, host_dst, dst_bytes);
   } catch (const std::bad_alloc&) {

@@ -31,6 +31,7 @@
 #include "../../include/gts.h"
 #include "blob_format.h"
 #include "nodal.cuh"
+#include "trace.h"
 #include "warp_bins.cuh"
 
 namespace gts {
@@ -100,6 +101,13 @@ __global__ void mirror_kernel(T* __restrict__ phi, int64_t n_mats, int M1) {
     __syncthreads();
   }
 }
+
+#ifndef GTS_GROUP_MAJOR
+#define GTS_GROUP_MAJOR 1  // group-major blocks: 0 never, 1 per-chunk slot maps (wide models), 2 whenever G > 1
+#endif
+#ifndef GTS_L2_BUDGET_MB
+#define GTS_L2_BUDGET_MB 32  // rows in flight keep X + phi (phi_ij) under this many MiB of L2
+#endif
 
 #ifndef GTS_INTER_MIRROR
 #define GTS_INTER_MIRROR 1  // per-chunk slot maps: upper-triangle atomics + mirror pass
@@ -184,24 +192,40 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   per_sm = std::max(per_sm, 1);
-  const int64_t row_tiles = (n_rows + W * 32 * R - 1) / (W * 32 * R);
+  const int64_t rows_per_block = (int64_t)W * 32 * R;
+  const int64_t row_tiles = (n_rows + rows_per_block - 1) / rows_per_block;
   const int64_t resident = (int64_t)num_sms() * per_sm;
   const int64_t target = resident * 2;
-  int64_t splits = (target + row_tiles - 1) / row_tiles;
-  {
+  const int64_t M1 = info->n_features + 1;
+  const int64_t l2_budget = (int64_t)GTS_L2_BUDGET_MB << 20;
+  const int G = info->n_groups;
+  // Group-major blocks (Args::n_bgroups) for per-chunk slot maps: the gathers
+  // re-read X and the flush REDs hit phi (phi_ij) once per chunk, so the rows
+  // in flight must keep their X rows and phi rows in L2.  Blocks are dispatched
+  // in index order, so with (batch, group, tile, split) order the resident
+  // blocks share one batch of rows and one group: tiles_per_batch is sized so
+  // that a batch's X and one group's outputs fit the L2 budget.
+  const bool wide = info->max_slots < info->n_features;
+  const int nbg = (G > 1 && (GTS_GROUP_MAJOR == 2 || (GTS_GROUP_MAJOR == 1 && wide))) ? G : 1;
+  int64_t tiles_per_batch = std::max<int64_t>(row_tiles, 1), splits;
+  if (nbg > 1) {
+    const int64_t bytes_per_row = (int64_t)sizeof(T) * (info->n_features + (kInter ? M1 * M1 : M1));
+    tiles_per_batch = std::max<int64_t>(1, std::min<int64_t>(tiles_per_batch,
+                                                             l2_budget / (rows_per_block * bytes_per_row)));
+    splits = (target + tiles_per_batch - 1) / tiles_per_batch;
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, info->n_units / G));
+  } else {
+    splits = (target + row_tiles - 1) / row_tiles;
     // Blocks run in index order (row tile major, split minor), so the first
     // `resident` blocks cover resident / splits row tiles.  Keep the rows in
     // flight small enough that their X rows and one group's phi (phi_ij) rows
-    // stay in L2 (wide models: the chunk gathers re-read X and the flush REDs
-    // hit phi once per chunk); splits only add one flush per split boundary.
-    const int64_t M1 = info->n_features + 1;
+    // stay in L2; splits only add one flush per split boundary.
     const int64_t bytes_per_row = (int64_t)sizeof(T) * (info->n_features + (kInter ? M1 * M1 : M1));
-    const int64_t l2_budget = 32ll << 20;
-    const int64_t rows_per_block = (int64_t)W * 32 * R;
     const int64_t want = (resident * rows_per_block * bytes_per_row + l2_budget - 1) / l2_budget;
     splits = std::max(splits, std::min(want, row_tiles > 0 ? resident : 1));
   }
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, std::min<int64_t>(info->n_units, 1024)));
+  const int64_t n_batches = (row_tiles + tiles_per_batch - 1) / tiles_per_batch;
   nodal::Args a;
   a.blob = d_blob;
   a.X = d_X;
@@ -212,22 +236,23 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   a.out_phi = out_phi;
   a.upper_only = kInter && uses_mirror(info);
   a.n_splits = (int)splits;
+  a.n_bgroups = nbg;
+  a.tiles_per_batch = tiles_per_batch;
   a.tile_w = shap_tile_w(info);
   a.M = info->n_features;
   a.G = info->n_groups;
   a.n_chunks = info->n_units;
   a.max_chunk_bytes = (int)nodal_buffer_bytes(info);
   if (info->n_units == 0) return GTS_OK;
-  const int64_t blocks = row_tiles * splits;
+  const int64_t blocks = n_batches * nbg * tiles_per_batch * splits;
   if (blocks > INT32_MAX) return fail(GTS_ERR_INVALID_ARGUMENT, "too many rows");
   kern<<<(unsigned)blocks, W * 32, smem, st>>>(a);
   gts_status s = cuda_check("nodal kernel launch");
   if (s != GTS_OK || !a.upper_only) return s;
-  const int M1 = info->n_features + 1;
   const int64_t nt = (M1 + 31) / 32;
   const int64_t tiles = n_rows * info->n_groups * (nt * (nt + 1) / 2);
   const int mblocks = (int)std::min<int64_t>(tiles, (int64_t)num_sms() * 16);
-  mirror_kernel<T><<<mblocks, dim3(32, 8), 0, st>>>(static_cast<T*>(out), n_rows * info->n_groups, M1);
+  mirror_kernel<T><<<mblocks, dim3(32, 8), 0, st>>>(static_cast<T*>(out), n_rows * info->n_groups, (int)M1);
   return cuda_check("mirror kernel launch");
 }
 
@@ -384,33 +409,39 @@ extern "C" {
 
 gts_status gts_shap(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows, int64_t ld_x,
                     void* d_phi, void* stream) {
+  GTS_NVTX("gts_shap");
   return gts::run<false>(info, d_blob, d_X, n_rows, ld_x, 1, d_phi, stream);
 }
 
 gts_status gts_shap_interactions(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
                                  int64_t ld_x, void* d_phi_ij, void* stream) {
+  GTS_NVTX("gts_shap_interactions");
   return gts::run<true>(info, d_blob, d_X, n_rows, ld_x, 1, d_phi_ij, stream);
 }
 
 gts_status gts_shap_strided(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
                             int64_t row_stride, int64_t col_stride, void* d_phi, void* stream) {
+  GTS_NVTX("gts_shap_strided");
   return gts::run<false>(info, d_blob, d_X, n_rows, row_stride, col_stride, d_phi, stream);
 }
 
 gts_status gts_shap_interactions_strided(const gts_blob_info* info, const void* d_blob, const void* d_X,
                                          int64_t n_rows, int64_t row_stride, int64_t col_stride, void* d_phi_ij,
                                          void* stream) {
+  GTS_NVTX("gts_shap_interactions_strided");
   return gts::run<true>(info, d_blob, d_X, n_rows, row_stride, col_stride, d_phi_ij, stream);
 }
 
 gts_status gts_shap_and_interactions(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
                                      int64_t row_stride, int64_t col_stride, void* d_phi, void* d_phi_ij,
                                      void* stream) {
+  GTS_NVTX("gts_shap_and_interactions");
   return gts::run_fused(info, d_blob, d_X, n_rows, row_stride, col_stride, d_phi, d_phi_ij, stream);
 }
 
 gts_status gts_validate_x(gts_dtype dtype, const void* d_X, int64_t n_rows, int32_t n_features, int64_t row_stride,
                           int64_t col_stride, void* stream) {
+  GTS_NVTX("gts_validate_x");
   if (dtype != GTS_F32 && dtype != GTS_F64) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "bad dtype");
   if (n_rows < 0 || n_features < 1) return gts::fail(GTS_ERR_INVALID_ARGUMENT, "bad sizes");
   if (n_rows == 0) return GTS_OK;

@@ -916,6 +916,12 @@ struct Args {
   void* out_phi;  // interaction kernel only: if set, the phi_i cells are also added to phi (fused call)
   int upper_only;  // interaction kernel only: write cells (i, j) with i < j only; mirror_kernel fills (j, i)
   int n_splits;
+  // Block decomposition: blockIdx = ((batch * n_bgroups + g) * tiles_per_batch + tile) * n_splits + split.
+  // n_bgroups = 1: a block walks the chunks of every group (its split of them);
+  // n_bgroups = G: a block walks group g's chunks only, so the blocks resident
+  // at one time share one group's phi rows and the rows of one batch (L2 reuse).
+  int n_bgroups;
+  int64_t tiles_per_batch;
   int tile_w;  // SHAP: row stride of the X / phi tiles = widest slot map + 1 (odd)
   int M, G;
   int64_t n_chunks;
@@ -1040,15 +1046,34 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   T* const sT = reinterpret_cast<T*>(g_smem);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t row_tile = blockIdx.x / a.n_splits;
-  const int split = blockIdx.x % a.n_splits;
+  const int split = (int)(blockIdx.x % a.n_splits);
+  const int64_t bt = blockIdx.x / a.n_splits;                // (batch, group, tile)
+  const int64_t tile = bt % a.tiles_per_batch, bg = bt / a.tiles_per_batch;
+  const int64_t batch = bg / a.n_bgroups;
+  const int bgroup = (int)(bg % a.n_bgroups);
+  const int64_t row_tile = batch * a.tiles_per_batch + tile;
   const int64_t row0 = row_tile * (W * ROWS) + (int64_t)warp * ROWS;
+  if (row_tile * (W * ROWS) >= a.n_rows) return;  // padding tile of the last batch (uniform per block)
 
-  const double wtot = work[a.n_chunks];
+  // this block's chunk range: all chunks, or group bgroup's (chunks are in group order)
+  int64_t g_lo = 0, g_hi = a.n_chunks;
+  if (a.n_bgroups > 1) {
+    auto first_of = [&](int g) -> int64_t {  // first chunk with group >= g
+      int64_t lo = 0, hi = a.n_chunks;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (chunks[mid].group < g) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    g_lo = first_of(bgroup);
+    g_hi = first_of(bgroup + 1);
+  }
+  const double w_lo = work[g_lo], w_span = work[g_hi] - w_lo;
   auto split_begin = [&](int s) -> int64_t {
-    if (s >= a.n_splits) return a.n_chunks;
-    const double target = wtot * (double)s / (double)a.n_splits;
-    int64_t lo = 0, hi = a.n_chunks;  // first c with work[c] >= target
+    if (s >= a.n_splits) return g_hi;
+    const double target = w_lo + w_span * (double)s / (double)a.n_splits;
+    int64_t lo = g_lo, hi = g_hi;  // first c with work[c] >= target
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
       if (work[mid] < target) lo = mid + 1; else hi = mid;
