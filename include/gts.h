@@ -219,6 +219,15 @@ gts_status gts_blob_plan_for(const gts_bins* bins, gts_dtype dtype, gts_layout l
 /* Serialise into caller HOST memory of at least info->bytes (any alignment
    >= 16).  The caller copies the bytes to a device buffer (16-byte aligned). */
 gts_status gts_blob_write(const gts_bins* bins, const gts_blob_info* info, void* host_dst, size_t dst_bytes);
+/* Bytes [offset, offset + bytes) of the same blob into caller HOST memory
+   (host_dst receives exactly `bytes` bytes), so a large blob can be streamed
+   host -> device through small pinned buffers while the next range is being
+   written.  Writing every range once gives the bytes
+   of gts_blob_write.  The plan of the preceding gts_blob_plan* call is kept
+   between ranges (gts_blob_write frees it).  Errors: INVALID_ARGUMENT (range
+   outside [0, info->bytes), info not of these bins). */
+gts_status gts_blob_write_range(const gts_bins* bins, const gts_blob_info* info, int64_t offset, int64_t bytes,
+                                void* host_dst);
 
 /* ---------------------------------------------------------- (3)/(4) compute */
 

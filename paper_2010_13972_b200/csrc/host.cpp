@@ -43,15 +43,33 @@ const char* last_error() { return g_last_error.c_str(); }
 
 // ------------------------------------------------------------- path table
 
+// Allocator whose resize() leaves new elements uninitialised: the big table
+// arrays are filled by parallel loops (first touch spread over the threads)
+// instead of being zeroed by one thread first.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind { using other = NoInitAlloc<U>; };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept { ::new (static_cast<void*>(p)) U; }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) { ::new (static_cast<void*>(p)) U(std::forward<A>(a)...); }
+};
+template <class T>
+using big_vector = std::vector<T, NoInitAlloc<T>>;
+
 struct PathTable {
   int32_t n_features = 0, n_groups = 0, max_len = 0;
   double base_score = 0.0;
-  std::vector<int64_t> path_offset;
-  std::vector<int32_t> feature;
-  std::vector<float> lower, upper;
-  std::vector<double> zero_fraction;
-  std::vector<double> v;
-  std::vector<int32_t> group, tree;
+  big_vector<int64_t> path_offset;
+  big_vector<int32_t> feature;
+  big_vector<float> lower, upper;
+  big_vector<double> zero_fraction;
+  big_vector<double> v;
+  big_vector<int32_t> group, tree;
   std::vector<double> bias;
   int64_t n_paths() const { return (int64_t)v.size(); }
   int64_t n_elems() const { return (int64_t)feature.size(); }
@@ -290,12 +308,18 @@ static gts_status extract(const gts_model* m, std::shared_ptr<PathTable>& out) {
   tab->path_offset[L] = E;
   // bias (a5, reading G13): sum over paths in path order of v * prod z (table
   // order), fp64; base_score added last.
+  // The per-path products are independent (computed in parallel, each in
+  // table order); the sum runs serially in path order, so the result is the
+  // same bit pattern as one serial loop.
   tab->bias.assign(m->n_groups, 0.0);
+  std::vector<double> vprod(L);
+#pragma omp parallel for schedule(static)
   for (int64_t p = 0; p < L; ++p) {
     double prod = 1.0;
     for (int64_t e = tab->path_offset[p]; e < tab->path_offset[p + 1]; ++e) prod *= tab->zero_fraction[e];
-    tab->bias[tab->group[p]] += tab->v[p] * prod;
+    vprod[p] = tab->v[p] * prod;
   }
+  for (int64_t p = 0; p < L; ++p) tab->bias[tab->group[p]] += vprod[p];
   for (int32_t g = 0; g < m->n_groups; ++g) tab->bias[g] += m->base_score;
   out = std::move(tab);
   return GTS_OK;
@@ -942,60 +966,64 @@ static void write_gauss(char* dst) {
 // nodal tables, computed in fp64 from the fp64 zero fractions and leaf values
 // and rounded once to T (reading G11: one rounding in fp32 mode).  Per node the
 // reciprocals 1/A_sq and 1/(1 - t_q) are formed once and multiplied.
-template <typename T>
-static void write_regions(const PathTable& tab, const NodalPlan& np, int S, int nt, char* out) {
+struct GaussTab {  // Q-point rules on [0, 1] for Q = 1..kQMax, in fp64
   double tq[kQMax + 1][kQMax], wq[kQMax + 1][kQMax], rq[kQMax + 1][kQMax];
-  for (int Q = 1; Q <= kQMax; ++Q) {
-    long double t[kQMax], w[kQMax];
-    gauss_legendre01(Q, t, w);
-    for (int q = 0; q < Q; ++q) {
-      tq[Q][q] = (double)t[q];
-      wq[Q][q] = (double)w[q];
-      rq[Q][q] = (double)(1.0L / (1.0L - t[q]));
+  GaussTab() {
+    for (int Q = 1; Q <= kQMax; ++Q) {
+      long double t[kQMax], w[kQMax];
+      gauss_legendre01(Q, t, w);
+      for (int q = 0; q < Q; ++q) {
+        tq[Q][q] = (double)t[q];
+        wq[Q][q] = (double)w[q];
+        rq[Q][q] = (double)(1.0L / (1.0L - t[q]));
+      }
     }
   }
-  const int64_t C = (int64_t)np.chunks.size();
-#pragma omp parallel for schedule(dynamic, 16)
-  for (int64_t ci = 0; ci < C; ++ci) {
-    const ChunkRec& c = np.chunks[ci];
-    char* region = out + c.data_off;
-    int32_t* E = reinterpret_cast<int32_t*>(region);
-    int32_t* Pp = E + 4 * (int64_t)c.n_elems;
-    T* tab_out = reinterpret_cast<T*>(Pp + 4 * (int64_t)c.n_paths);
-    for (int32_t p = 0; p < c.n_paths; ++p) {
-      const PathRec& pr = np.paths[c.path_begin + p];
-      Pp[4 * p + 0] = pr.k;
-      Pp[4 * p + 1] = pr.q;
-      Pp[4 * p + 2] = pr.elem;
-      Pp[4 * p + 3] = pr.table;
-      const int k = pr.k & 0xff, Q = pr.q, QP = nodal_qp(Q);
-      const int64_t e0 = tab.path_offset[pr.src] + 1;  // first non-root element
-      const uint8_t* sl = &np.slots[c.elem_begin + pr.elem];
+};
+
+// The staged region of chunk ci, written at `region` (c.data_bytes bytes;
+// table pads q >= Q and the tail stay zero).
+template <typename T>
+static void write_region(const PathTable& tab, const NodalPlan& np, const GaussTab& gt, int64_t ci, int S, int nt,
+                         char* region) {
+  const ChunkRec& c = np.chunks[ci];
+  std::memset(region, 0, (size_t)c.data_bytes);
+  int32_t* E = reinterpret_cast<int32_t*>(region);
+  int32_t* Pp = E + 4 * (int64_t)c.n_elems;
+  T* tab_out = reinterpret_cast<T*>(Pp + 4 * (int64_t)c.n_paths);
+  for (int32_t p = 0; p < c.n_paths; ++p) {
+    const PathRec& pr = np.paths[c.path_begin + p];
+    Pp[4 * p + 0] = pr.k;
+    Pp[4 * p + 1] = pr.q;
+    Pp[4 * p + 2] = pr.elem;
+    Pp[4 * p + 3] = pr.table;
+    const int k = pr.k & 0xff, Q = pr.q, QP = nodal_qp(Q);
+    const int64_t e0 = tab.path_offset[pr.src] + 1;  // first non-root element
+    const uint8_t* sl = &np.slots[c.elem_begin + pr.elem];
+    for (int s = 0; s < k; ++s) {
+      int32_t* rec = E + 4 * (int64_t)(pr.elem + s);
+      std::memcpy(&rec[0], &tab.lower[e0 + s], 4);
+      std::memcpy(&rec[1], &tab.upper[e0 + s], 4);
+      rec[2] = sl[s];
+      rec[3] = sl[s] * (2 * S - sl[s] - 1) / 2;  // upper-triangle row base of the slot
+    }
+    const double* z = &tab.zero_fraction[e0];
+    const double v = tab.v[pr.src];
+    T* t = tab_out + pr.table;
+    for (int q = 0; q < Q; ++q) {
+      const double tt = gt.tq[Q][q], w = gt.wq[Q][q], r1 = gt.rq[Q][q];
+      double cq = 1.0;
+      for (int s = 0; s < k; ++s) cq *= z[s] + (1.0 - z[s]) * tt;
+      t[q] = (T)cq;
+      t[QP + q] = (T)(-v * w * r1);
+      if (nt == 3) t[2 * QP + q] = (T)(0.5 * v * w);
       for (int s = 0; s < k; ++s) {
-        int32_t* rec = E + 4 * (int64_t)(pr.elem + s);
-        std::memcpy(&rec[0], &tab.lower[e0 + s], 4);
-        std::memcpy(&rec[1], &tab.upper[e0 + s], 4);
-        rec[2] = sl[s];
-        rec[3] = sl[s] * (2 * S - sl[s] - 1) / 2;  // upper-triangle row base of the slot
-      }
-      const double* z = &tab.zero_fraction[e0];
-      const double v = tab.v[pr.src];
-      T* t = tab_out + pr.table;
-      for (int q = 0; q < Q; ++q) {
-        const double tt = tq[Q][q], w = wq[Q][q], r1 = rq[Q][q];
-        double cq = 1.0;
-        for (int s = 0; s < k; ++s) cq *= z[s] + (1.0 - z[s]) * tt;
-        t[q] = (T)cq;
-        t[QP + q] = (T)(-v * w * r1);
-        if (nt == 3) t[2 * QP + q] = (T)(0.5 * v * w);
-        for (int s = 0; s < k; ++s) {
-          const double zs = z[s];
-          const double A = zs + (1.0 - zs) * tt, iA = 1.0 / A;
-          T* row = t + nt * QP + s * nt * QP;
-          row[q] = (T)(zs * (1.0 - tt) * iA);                 // rho = B / A
-          row[QP + q] = (T)(v * w * ((1.0 - zs) * iA + r1));  // C' = C - d
-          if (nt == 3) row[2 * QP + q] = (T)((1.0 - zs) * iA);
-        }
+        const double zs = z[s];
+        const double A = zs + (1.0 - zs) * tt, iA = 1.0 / A;
+        T* row = t + nt * QP + s * nt * QP;
+        row[q] = (T)(zs * (1.0 - tt) * iA);                 // rho = B / A
+        row[QP + q] = (T)(v * w * ((1.0 - zs) * iA + r1));  // C' = C - d
+        if (nt == 3) row[2 * QP + q] = (T)((1.0 - zs) * iA);
       }
     }
   }
@@ -1070,52 +1098,138 @@ static gts_status blob_plan_cached(const gts_bins* b, int32_t dtype, int32_t lay
   return GTS_OK;
 }
 
-static gts_status blob_write(const gts_bins* b, const gts_blob_info* info, void* dst, size_t dst_bytes) {
-  if (!b || !info || !dst) return fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
+// Bytes [offset, offset + len) of the blob into dst.  The plan of the last
+// gts_blob_plan* call on these bins is used when it matches `info` (taken when
+// `take`, i.e. by a whole-blob gts_blob_write; kept for the next range
+// otherwise), else the plan is rebuilt (a pure function of the bins and the
+// info's dtype / layout / slots / uses).
+static gts_status blob_write_range(const gts_bins* b, const gts_blob_info* info, int64_t offset, int64_t len,
+                                   void* dst, bool take) {
+  if (!b || !info || (!dst && len > 0)) return fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
   if (info->magic != kMagic || info->abi_version != GTS_ABI_VERSION)
     return fail(GTS_ERR_INVALID_ARGUMENT, "info is not a gts_blob_info of ABI version %d", GTS_ABI_VERSION);
+  if (offset < 0 || len < 0 || offset + len > info->bytes)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "range [%lld, %lld) outside the %lld-byte blob", (long long)offset,
+                (long long)(offset + len), (long long)info->bytes);
   std::shared_ptr<PlanCache> pc;
   {
     std::lock_guard<std::mutex> lock(b->cache_mu);
-    if (b->cache && std::memcmp(&b->cache->info, info, sizeof(*info)) == 0) pc = std::move(b->cache);
+    if (b->cache && std::memcmp(&b->cache->info, info, sizeof(*info)) == 0) {
+      pc = b->cache;
+      if (take) b->cache.reset();
+    }
   }
-  if (!pc) {  // re-plan: the blob's shape is a pure function of (bins, dtype, layout, slots, uses)
+  if (!pc) {
     pc = std::make_shared<PlanCache>();
-    gts_blob_info fresh;
     const int32_t req_uses = info->layout == GTS_LAYOUT_NODAL ? info->uses : 0;
-    gts_status st = blob_plan(b, info->dtype, info->layout, info->max_slots, req_uses, &fresh, &pc->hdr, &pc->np,
+    gts_status st = blob_plan(b, info->dtype, info->layout, info->max_slots, req_uses, &pc->info, &pc->hdr, &pc->np,
                               &pc->bp);
     if (st != GTS_OK) return st;
-    if (fresh.bytes != info->bytes || fresh.n_units != info->n_units || fresh.n_tables != info->n_tables)
+    if (pc->info.bytes != info->bytes || pc->info.n_units != info->n_units || pc->info.n_tables != info->n_tables)
       return fail(GTS_ERR_INVALID_ARGUMENT, "blob info does not match these bins");
+    pc->dtype = info->dtype;
+    pc->layout = info->layout;
+    pc->max_slots = info->max_slots;
+    pc->uses = req_uses;
+    if (!take) {
+      std::lock_guard<std::mutex> lock(b->cache_mu);
+      b->cache = pc;
+    }
   }
   const BlobHeader& h = pc->hdr;
-  if (dst_bytes < (size_t)h.bytes)
-    return fail(GTS_ERR_INVALID_ARGUMENT, "destination too small: %zu < %lld", dst_bytes, (long long)h.bytes);
   char* out = static_cast<char*>(dst);
-  std::memset(out, 0, (size_t)h.bytes);
-  std::memcpy(out, &h, sizeof(h));
-  std::memcpy(out + h.off_bias, b->tab->bias.data(), 8 * b->tab->bias.size());
-  if (h.layout == GTS_LAYOUT_NODAL) {
-    const NodalPlan& np = pc->np;
-    if (h.dtype == GTS_F32) write_gauss<float>(out + h.off_gauss);
-    else write_gauss<double>(out + h.off_gauss);
-    std::memcpy(out + h.off_units, np.chunks.data(), sizeof(ChunkRec) * np.chunks.size());
-    double* ws = reinterpret_cast<double*>(out + h.off_work);
+  const int64_t end = offset + len;
+  if (h.layout != GTS_LAYOUT_NODAL) {  // WARP_BINS: the whole blob, then the range
+    std::vector<char> full;
+    char* w = out;
+    if (offset != 0 || len != h.bytes) {
+      full.assign((size_t)h.bytes, 0);
+      w = full.data();
+    } else {
+      std::memset(w, 0, (size_t)h.bytes);
+    }
+    std::memcpy(w, &h, sizeof(h));
+    std::memcpy(w + h.off_bias, b->tab->bias.data(), 8 * b->tab->bias.size());
+    if (h.dtype == GTS_F32) write_bins<float>(*b, pc->bp, h, w);
+    else write_bins<double>(*b, pc->bp, h, w);
+    if (w != out) std::memcpy(out, w + offset, (size_t)len);
+    return GTS_OK;
+  }
+  const NodalPlan& np = pc->np;
+  // head: header, bias, Gauss table, chunk records, prefix work, slot maps
+  if (offset < h.off_elems) {
+    std::vector<char> head((size_t)h.off_elems, 0);
+    char* w = head.data();
+    std::memcpy(w, &h, sizeof(h));
+    std::memcpy(w + h.off_bias, b->tab->bias.data(), 8 * b->tab->bias.size());
+    if (h.dtype == GTS_F32) write_gauss<float>(w + h.off_gauss);
+    else write_gauss<double>(w + h.off_gauss);
+    std::memcpy(w + h.off_units, np.chunks.data(), sizeof(ChunkRec) * np.chunks.size());
+    double* ws = reinterpret_cast<double*>(w + h.off_work);
     double* wi = ws + (h.n_units + 1);
     ws[0] = wi[0] = 0;
     for (int64_t c = 0; c < h.n_units; ++c) {
       ws[c + 1] = ws[c] + np.work_shap[c];
       wi[c + 1] = wi[c] + np.work_inter[c];
     }
-    std::memcpy(out + h.off_slotmap, np.slotmap.data(), 4 * np.slotmap.size());
-    if (h.dtype == GTS_F32) write_regions<float>(*b->tab, np, h.max_slots, h.n_tables, out);
-    else write_regions<double>(*b->tab, np, h.max_slots, h.n_tables, out);
-  } else {
-    if (h.dtype == GTS_F32) write_bins<float>(*b, pc->bp, h, out);
-    else write_bins<double>(*b, pc->bp, h, out);
+    std::memcpy(w + h.off_slotmap, np.slotmap.data(), 4 * np.slotmap.size());
+    const int64_t e = std::min<int64_t>(end, h.off_elems);
+    std::memcpy(out, w + offset, (size_t)(e - offset));
   }
+  // staged chunk regions (back to back from off_elems), then zero padding to h.bytes
+  const int64_t C = (int64_t)np.chunks.size();
+  int64_t c0 = 0, c1 = C;
+  {
+    int64_t lo = 0, hi = C;  // first chunk ending after offset
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (np.chunks[mid].data_off + np.chunks[mid].data_bytes <= offset) lo = mid + 1; else hi = mid;
+    }
+    c0 = lo;
+    lo = c0, hi = C;  // first chunk starting at or after end
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (np.chunks[mid].data_off < end) lo = mid + 1; else hi = mid;
+    }
+    c1 = lo;
+  }
+  const GaussTab gt;
+  const int S = h.max_slots, nt = h.n_tables;
+#pragma omp parallel
+  {
+    std::vector<char> tmp;
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t ci = c0; ci < c1; ++ci) {
+      const ChunkRec& c = np.chunks[ci];
+      const int64_t a = c.data_off, z = c.data_off + c.data_bytes;
+      char* reg;
+      if (a >= offset && z <= end) {
+        reg = out + (a - offset);
+      } else {
+        tmp.resize((size_t)c.data_bytes);
+        reg = tmp.data();
+      }
+      if (h.dtype == GTS_F32) write_region<float>(*b->tab, np, gt, ci, S, nt, reg);
+      else write_region<double>(*b->tab, np, gt, ci, S, nt, reg);
+      if (reg != out + (a - offset)) {
+        const int64_t s0 = std::max(a, offset), s1 = std::min(z, end);
+        std::memcpy(out + (s0 - offset), reg + (s0 - a), (size_t)(s1 - s0));
+      }
+    }
+  }
+  const int64_t regions_end = C > 0 ? np.chunks[C - 1].data_off + np.chunks[C - 1].data_bytes : h.off_elems;
+  const int64_t p0 = std::max(offset, regions_end);
+  if (end > p0) std::memset(out + (p0 - offset), 0, (size_t)(end - p0));
   return GTS_OK;
+}
+
+static gts_status blob_write(const gts_bins* b, const gts_blob_info* info, void* dst, size_t dst_bytes) {
+  if (!b || !info || !dst) return fail(GTS_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (info->magic != kMagic || info->abi_version != GTS_ABI_VERSION)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "info is not a gts_blob_info of ABI version %d", GTS_ABI_VERSION);
+  if (dst_bytes < (size_t)info->bytes)
+    return fail(GTS_ERR_INVALID_ARGUMENT, "destination too small: %zu < %lld", dst_bytes, (long long)info->bytes);
+  return blob_write_range(b, info, 0, info->bytes, dst, true);
 }
 
 }  // namespace gts
@@ -1216,6 +1330,16 @@ gts_status gts_blob_write(const gts_bins* bins, const gts_blob_info* info, void*
   GTS_NVTX("gts_blob_write");
   try {
     return gts::blob_write(bins, info, host_dst, dst_bytes);
+  } catch (const std::bad_alloc&) {
+    return gts::fail(GTS_ERR_OUT_OF_MEMORY, "out of host memory");
+  }
+}
+
+gts_status gts_blob_write_range(const gts_bins* bins, const gts_blob_info* info, int64_t offset, int64_t bytes,
+                                void* host_dst) {
+  GTS_NVTX("gts_blob_write_range");
+  try {
+    return gts::blob_write_range(bins, info, offset, bytes, host_dst, false);
   } catch (const std::bad_alloc&) {
     return gts::fail(GTS_ERR_OUT_OF_MEMORY, "out of host memory");
   }

@@ -31,11 +31,37 @@ class Blob:
     def from_bins(cls, bins: gts.Bins, dtype: int, layout, max_slots: int, device) -> "Blob":
         return cls.from_info(bins, gts.gts_blob_plan(bins, dtype, layout, max_slots), device)
 
+    STREAM_PIECE = 64 << 20  # bytes per pinned staging buffer when streaming a blob to the device
+
     @classmethod
     def from_info(cls, bins: gts.Bins, info: gts.gts_blob_info, device) -> "Blob":
-        host = torch.empty(info.bytes, dtype=torch.uint8, pin_memory=torch.cuda.is_available())
-        gts.gts_blob_write(bins, info, host.numpy())
-        dev = host.to(device, non_blocking=True) if device is not None else host
+        """Serialise the blob and place it on `device`.  Blobs larger than two
+        staging pieces are streamed: range i is written on the host into one of
+        two pinned buffers while range i-1 is copied H2D on a side stream, so
+        the write overlaps the transfer and no blob-sized pinned buffer is
+        needed (gts_blob_write_range)."""
+        n = int(info.bytes)
+        on_gpu = device is not None and torch.device(device).type == "cuda"
+        if not on_gpu or n <= 2 * cls.STREAM_PIECE:
+            host = torch.empty(n, dtype=torch.uint8, pin_memory=torch.cuda.is_available())
+            gts.gts_blob_write(bins, info, host.numpy())
+            dev = host.to(device, non_blocking=True) if device is not None else host
+            return cls(info, dev)
+        dev = torch.empty(n, dtype=torch.uint8, device=device)
+        piece = cls.STREAM_PIECE
+        bufs = [torch.empty(piece, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        done = [None, None]
+        side = torch.cuda.Stream(device)
+        for i, off in enumerate(range(0, n, piece)):
+            j, m = i & 1, min(piece, n - off)
+            if done[j] is not None:
+                done[j].synchronize()  # the copy out of this buffer has finished
+            gts.gts_blob_write_range(bins, info, off, m, bufs[j].numpy())
+            with torch.cuda.stream(side):
+                dev[off:off + m].copy_(bufs[j][:m], non_blocking=True)
+                done[j] = torch.cuda.Event()
+                done[j].record(side)
+        side.synchronize()
         return cls(info, dev)
 
     _seq = 0  # broadcasts issued by this process (same order on every rank)

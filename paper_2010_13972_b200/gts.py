@@ -79,7 +79,7 @@ class gts_blob_info(ctypes.Structure):
 
 # The symbols the header declares (checked by tests/test_abi.py).
 EXPORTS = ["gts_extract_paths", "gts_paths_view_get", "gts_paths_free", "gts_binpack", "gts_bins_view_get",
-           "gts_bins_free", "gts_blob_plan", "gts_blob_plan_for", "gts_blob_write", "gts_shap", "gts_shap_interactions",
+           "gts_bins_free", "gts_blob_plan", "gts_blob_plan_for", "gts_blob_write", "gts_blob_write_range", "gts_shap", "gts_shap_interactions",
            "gts_shap_strided", "gts_shap_interactions_strided", "gts_shap_and_interactions",
            "gts_validate_x", "gts_launches_per_call", "gts_last_error", "gts_status_string", "gts_abi_version"]
 
@@ -107,6 +107,7 @@ def load(path: str = LIB_PATH):
     lib.gts_blob_plan.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _i32, P(gts_blob_info)]
     lib.gts_blob_plan_for.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _i32, ctypes.c_int, P(gts_blob_info)]
     lib.gts_blob_write.argtypes = [_vp, P(gts_blob_info), _vp, ctypes.c_size_t]
+    lib.gts_blob_write_range.argtypes = [_vp, P(gts_blob_info), _i64, _i64, _vp]
     for name in ("gts_shap", "gts_shap_interactions"):
         fn = getattr(lib, name)
         fn.argtypes = [P(gts_blob_info), _vp, _vp, _i64, _i64, _vp, _vp]
@@ -128,7 +129,7 @@ def load(path: str = LIB_PATH):
     lib.gts_abi_version.restype = _i32
     for name in ("gts_extract_paths", "gts_paths_view_get", "gts_binpack", "gts_bins_view_get", "gts_blob_plan",
                  "gts_blob_plan_for",
-                 "gts_blob_write", "gts_shap", "gts_shap_interactions"):
+                 "gts_blob_write", "gts_blob_write_range", "gts_shap", "gts_shap_interactions"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -247,6 +248,15 @@ def gts_blob_write(bins: Bins, info: gts_blob_info, dst=None) -> np.ndarray:
         raise ValueError("destination too small")
     _check(load().gts_blob_write(bins.handle, ctypes.byref(info), dst.ctypes.data, dst.nbytes))
     return dst
+
+
+def gts_blob_write_range(bins: Bins, info: gts_blob_info, offset: int, nbytes: int, dst) -> None:
+    """Bytes [offset, offset + nbytes) of the blob into ``dst`` (a uint8 host
+    array of at least nbytes, or a raw address)."""
+    ptr = dst if isinstance(dst, int) else dst.ctypes.data
+    if not isinstance(dst, int) and dst.nbytes < nbytes:
+        raise ValueError("destination too small")
+    _check(load().gts_blob_write_range(bins.handle, ctypes.byref(info), int(offset), int(nbytes), ptr))
 
 
 def gts_shap(info: gts_blob_info, d_blob: int, d_x: int, n_rows: int, ld_x: int, d_phi: int, stream: int = 0):

@@ -192,3 +192,30 @@ def test_product_path_fails_loudly_without_library(tmp_path):
             "gts.load(%r)" % (ROOT, str(tmp_path / "missing.so")))
     r = subprocess.run(["python", "-c", code], capture_output=True, text=True)
     assert r.returncode != 0 and "native library missing" in r.stderr
+
+
+@pytest.mark.parametrize("name,layout,uses", [("cal_housing-med", "nodal", "shap"), ("fashion_mnist-med", "nodal", "shap"),
+                                              ("fashion_mnist-med", "nodal", "interactions"),
+                                              ("cal_housing-small", "warp_bins", "shap")])
+def test_blob_write_range_pieces_equal_whole(name, layout, uses):
+    """gts_blob_write_range: any cut of [0, bytes) into ranges reproduces the
+    bytes of gts_blob_write (head, chunk regions split mid-record, tail pad)."""
+    from synth.configs import WORKLOADS
+    w = WORKLOADS[name]
+    ens = w.ensemble() if name != "fashion_mnist-med" else w.ensemble().subset(range(120))
+    b = gts.gts_binpack(gts.gts_extract_paths(ens), 32, "bfd")
+    info = gts.gts_blob_plan_for(b, gts.GTS_F32, layout, 0, uses)
+    whole = gts.gts_blob_write(b, info)
+    rng = np.random.default_rng(7)
+    for piece in (4096, 1000, 77777, int(info.bytes)):
+        got = np.full(info.bytes, 0xAB, np.uint8)
+        off = 0
+        while off < info.bytes:
+            m = int(min(info.bytes - off, max(1, piece + rng.integers(-piece // 2, piece // 2 + 1))))
+            buf = np.empty(m, np.uint8)
+            gts.gts_blob_write_range(b, info, off, m, buf)
+            got[off:off + m] = buf
+            off += m
+        assert np.array_equal(got, whole), piece
+    with pytest.raises(gts.GtsError):
+        gts.gts_blob_write_range(b, info, info.bytes - 4, 8, np.empty(8, np.uint8))
