@@ -535,15 +535,26 @@ def run_ours(args):
         xa = run.xd[:na]
         res = {"rows": na, "layout": "warp_bins (paper lineage: lane per path element, shuffles, swap-to-end)"}
 
-        def timed1(fn, x):
-            fn(x)
+        def timed1(fn, x, target_s=4.0):
+            """rows/s of fn on a prefix of x sized for ~target_s of device time
+            (a 256-row probe first: the paper-lineage kernel is ~50x slower)."""
+            def once(xx):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(run.stream)
+                fn(xx)
+                b.record(run.stream)
+                torch.cuda.synchronize()
+                return a.elapsed_time(b) / 1000.0
+            probe = x[:min(256, x.shape[0])]
+            fn(probe)
             torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(run.stream)
-            fn(x)
-            b.record(run.stream)
+            rate = probe.shape[0] / max(once(probe), 1e-6)
+            m = int(min(x.shape[0], max(probe.shape[0], rate * target_s)))
+            xx = x[:m]
+            fn(xx)
             torch.cuda.synchronize()
-            return x.shape[0] / (a.elapsed_time(b) / 1000.0)
+            res["timed_rows"] = m
+            return m / once(xx)
 
         packs = ["bfd", "ffd", "nf", "none"] if args.pack_ablation else [args.pack]
         for pk in packs:

@@ -40,6 +40,9 @@
                                                 // Q = 3 (pair + scalar tail) -4 %, padded to 4 nodes -14 %
                                                 // (profiles/r01n, r01i)
 #endif
+#ifndef GTS_INTER_REGACC
+#define GTS_INTER_REGACC 0  // bit Q: interaction runs with Q nodes keep the run's pair cells in registers
+#endif
 #ifndef GTS_X2_R2_QMAX
 #define GTS_X2_R2_QMAX 6  // largest Q whose paired-node SHAP run keeps both rows of a lane in flight
                           // (measured: adult SHAP +19 % for 6 over 4; profiles/r01h)
@@ -880,9 +883,12 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
                 inter_run<T, 4, 1, false>(k, n_run, E, tab, gam, xb1, ab1);
               }
               break;
-            case 5: inter_run<T, 5, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break;
+            case 5: inter_run<T, 5, 1, (GTS_INTER_REGACC & (1 << 5)) != 0>(k, n_run, E, tab, gam, xb1, ab1); break;
             case 6:
-              if constexpr (sizeof(T) == 4) { inter_run<T, 6, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break; }
+              if constexpr (sizeof(T) == 4) {
+                inter_run<T, 6, 1, (GTS_INTER_REGACC & (1 << 6)) != 0>(k, n_run, E, tab, gam, xb1, ab1);
+                break;
+              }
               [[fallthrough]];
             case 7:
               if constexpr (sizeof(T) == 4) {
@@ -951,6 +957,9 @@ __host__ __device__ constexpr int acc_stride(int tile_w) { return kInter ? (acc_
 // per-chunk maps of 32) trade warps for rows per lane: the per-path tables
 // are read from shared memory once per lane and used for R rows, which is
 // what bounds these kernels (LSU pipe, profiles/r01g).
+#ifndef GTS_INTER8_MINB
+#define GTS_INTER8_MINB 2  // resident blocks per SM the 8-slot fp32 interaction kernel's registers are sized for
+#endif
 #ifndef GTS_SHAP_R32
 #define GTS_SHAP_R32 1  // measured (profiles/r02b): R 1 / W 8 3.02e5 rows/s fashion, R 2 / W 4 2.49e5
 #endif
@@ -984,7 +993,8 @@ struct Cfg {
                            : tile_bytes * 2 <= 160 * 1024 ? 2
                                                           : 1;  // 32-slot interaction tiles (528 pair cells per row)
   static constexpr int kMinBlocks = (sizeof(T) == 4 && kWide) ? (S == 32 ? GTS_SHAP_B32 : GTS_SHAP_B64)
-                                                              : (W >= 8 ? 2 : 1);
+                                   : (sizeof(T) == 4 && kInter && S == 8) ? GTS_INTER8_MINB
+                                                                          : (W >= 8 ? 2 : 1);
 };
 
 // shared-memory layout: gauss (T) | X tiles (T) | phi tiles (T) | 2 staging buffers | 2 mbarriers
