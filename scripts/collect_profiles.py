@@ -3,7 +3,7 @@ the bench line, the ncu launch list with per-kernel shares, the ncu --set full
 summaries, test logs; and record per-launch DRAM traffic in profiles/traffic.json
 (read by bench.py for roofline.traffic).
 
-usage: python scripts/collect_profiles.py gpurun_out/r01a profiles/r01 [workload/layout/mode/dtype=kernelregex[@capture] ...]
+usage: python scripts/collect_profiles.py gpurun_out/r01a profiles/r01 [workload/layout/mode/dtype=kernelregex[@capture][#rows] ...]
 """
 import collections
 import csv
@@ -74,6 +74,7 @@ def main():
         tr = rep_traffic(os.path.join(src, rep))
         rep = rep[:-8] + ".ncu-rep" if rep.endswith(".raw.csv") else rep
         for key, rx in keys:
+            rx, _, rows = rx.partition("#")  # key=kernelregex[@capture][#rows]: rows per captured launch
             rx, _, only = rx.partition("@")  # key=kernelregex@capture: only that capture's kernels
             if only and not rep.startswith(only):
                 continue
@@ -82,6 +83,8 @@ def main():
                     traffic[key] = {"dram_bytes_per_launch": sum(vals) / len(vals), "kernel": kname,
                                     "source": f"{dst}/{rep[:-8]}.summary.txt (ncu --set full, dram__bytes_read.sum + "
                                               f"dram__bytes_write.sum)", "launches": len(vals)}
+                    if rows:
+                        traffic[key]["rows_per_launch"] = int(rows)
     json.dump(traffic, open(tfile, "w"), indent=1, sort_keys=True)
     print(open(tfile).read())
 
