@@ -133,6 +133,32 @@ __global__ void nonfinite_kernel(const T* __restrict__ X, int64_t n_rows, int M,
   }
 }
 
+// Feature-major copy of row-major X (xt[f * n + r] = X[r * rs + f]) for the
+// kernels that read X from global memory (nodal::xg_enabled): 32 x 32 tiles
+// through shared memory, coalesced on both sides.
+template <typename T>
+__global__ void transpose_x_kernel(const T* __restrict__ X, int64_t n, int M, int64_t rs, T* __restrict__ xt) {
+  __shared__ T tile[32][33];
+  const int64_t tiles_r = (n + 31) / 32;
+  const int tiles_f = (M + 31) / 32;
+  for (int64_t t = blockIdx.x; t < tiles_r * tiles_f; t += gridDim.x) {
+    const int64_t r0 = (t / tiles_f) * 32;
+    const int f0 = (int)(t % tiles_f) * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+      const int64_t r = r0 + y;
+      const int f = f0 + threadIdx.x;
+      if (r < n && f < M) tile[y][threadIdx.x] = X[r * rs + f];
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+      const int f = f0 + y;
+      const int64_t r = r0 + threadIdx.x;
+      if (r < n && f < M) xt[(int64_t)f * n + r] = tile[threadIdx.x][y];
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------- launchers
 
 constexpr int64_t kBiasOffset = 256;  // align256(sizeof(BlobHeader)), host.cpp blob_plan
@@ -189,6 +215,24 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   auto kern = nodal::nodal_kernel<T, S, W, R, kInter>;
   const size_t smem = nodal_smem_bytes<T, kInter, S>(info);
   if (smem > 227 * 1024) return fail(GTS_ERR_INVALID_ARGUMENT, "chunk staging needs %zu bytes of shared memory", smem);
+  void* xt = nullptr;  // feature-major scratch copy of a row-major X (xg kernels)
+  if (nodal::xg_enabled<kInter, S>() && rs != 1 && info->n_units > 0) {
+    const size_t bytes = (size_t)n_rows * info->n_features * sizeof(T);
+    if (cudaMallocAsync(&xt, bytes, st) != cudaSuccess)
+      return fail(GTS_ERR_OUT_OF_MEMORY, "cudaMallocAsync of %zu bytes for the feature-major X copy failed", bytes);
+    const int64_t tiles = ((n_rows + 31) / 32) * ((info->n_features + 31) / 32);
+    const int tb = (int)std::min<int64_t>(tiles, (int64_t)num_sms() * 16);
+    transpose_x_kernel<T><<<tb, dim3(32, 8), 0, st>>>(static_cast<const T*>(d_X), n_rows, info->n_features, rs,
+                                                       static_cast<T*>(xt));
+    gts_status s0 = cuda_check("X transpose launch");
+    if (s0 != GTS_OK) {
+      cudaFreeAsync(xt, st);
+      return s0;
+    }
+    d_X = xt;
+    rs = 1;
+    cs = n_rows;
+  }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
@@ -246,9 +290,13 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   a.max_chunk_bytes = (int)nodal_buffer_bytes(info);
   if (info->n_units == 0) return GTS_OK;
   const int64_t blocks = n_batches * nbg * tiles_per_batch * splits;
-  if (blocks > INT32_MAX) return fail(GTS_ERR_INVALID_ARGUMENT, "too many rows");
+  if (blocks > INT32_MAX) {
+    if (xt != nullptr) cudaFreeAsync(xt, st);
+    return fail(GTS_ERR_INVALID_ARGUMENT, "too many rows");
+  }
   kern<<<(unsigned)blocks, W * 32, smem, st>>>(a);
   gts_status s = cuda_check("nodal kernel launch");
+  if (xt != nullptr) cudaFreeAsync(xt, st);  // stream-ordered: after the kernel
   if (s != GTS_OK || !a.upper_only) return s;
   const int64_t nt = (M1 + 31) / 32;
   const int64_t tiles = n_rows * info->n_groups * (nt * (nt + 1) / 2);
@@ -480,7 +528,10 @@ int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions) {
   const int32_t mirror = gts::uses_mirror(info) ? 1 : 0;
   if (interactions == 2)  // gts_shap_and_interactions
     return info->layout == GTS_LAYOUT_NODAL ? 2 + main + mirror : 2 + 2 * main;
-  return 1 + main + (interactions ? mirror : 0);  // init + main kernel (+ mirror pass)
+  // SHAP kernels that read X from global memory transpose a row-major X first
+  const int32_t xt = (!interactions && info->layout == GTS_LAYOUT_NODAL && main &&
+                      info->max_slots >= GTS_XG_MIN_S) ? 1 : 0;
+  return 1 + main + (interactions ? mirror : xt);  // init + main kernel (+ mirror pass / X transpose)
 }
 
 }  // extern "C"

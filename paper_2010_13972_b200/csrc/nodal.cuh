@@ -113,6 +113,16 @@ __device__ __forceinline__ bool one_fraction(T x, int4 rec) {
   return (x >= (T)__int_as_float(rec.x)) & (x < (T)__int_as_float(rec.y));
 }
 
+// x value of lane-row xb at a slot: from the warp's shared X tile (xb = tile
+// row base), or, for kXg kernels, straight from feature-major X in global
+// memory (xb = the row; consecutive lanes read consecutive rows of one
+// feature: one coalesced, L1-resident line per warp instruction).
+template <typename T, bool kXg>
+__device__ __forceinline__ T load_x(const T* sT, int xb, int slot, const T* __restrict__ xg, int64_t cs) {
+  if constexpr (kXg) return __ldg(xg + (int64_t)slot * cs + xb);
+  else return sT[xb + slot];
+}
+
 // --------------------------------------------------------------------- SHAP
 
 // A run of n_run paths with one feature set; k in {2Q-1, 2Q}; fully unrolled.
@@ -121,9 +131,9 @@ __device__ __forceinline__ bool one_fraction(T x, int4 rec) {
 // i.e. an o_s = 1 element costs one predicated FMA chain straight into its
 // accumulator and an o_s = 0 element costs nothing; ph0 is summed once per
 // path into one register per row and added to every slot of the run at its end.
-template <typename T, int Q, int R, int NT>
+template <typename T, int Q, int R, int NT, bool kXg>
 __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restrict__ E, const T* __restrict__ tab,
-                                         const int (&xb)[R], const int (&ab)[R]) {
+                                         const int (&xb)[R], const int (&ab)[R], const T* __restrict__ xg, int64_t cs) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q;
   constexpr int kRmw = GTS_RMW_REGS / R > 1 ? GTS_RMW_REGS / R : 1;
   T* const sT = reinterpret_cast<T*>(g_smem);
@@ -138,7 +148,7 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = (T)0;
-      xv[r][s] = sT[xb[r] + slot[s]];
+      xv[r][s] = load_x<T, kXg>(sT, xb[r], slot[s], xg, cs);
     }
   }
   for (int p = 0; p < n_run; ++p) {
@@ -229,9 +239,10 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 // work), predicated per row as before.  Pads (q >= Q) are zero in the table,
 // so P_pad = 0 and they contribute nothing.  acc keeps even/odd node partial
 // sums, folded once per run.
-template <int Q, int R, int NT>
+template <int Q, int R, int NT, bool kXg>
 __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __restrict__ E,
-                                            const float* __restrict__ tab, const int (&xb)[R], const int (&ab)[R]) {
+                                            const float* __restrict__ tab, const int (&xb)[R], const int (&ab)[R],
+                                            const float* __restrict__ xg, int64_t cs) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q, QH = (Q + 1) / 2;
   constexpr int kRmw = GTS_RMW_REGS / R > 1 ? GTS_RMW_REGS / R : 1;
   float* const sT = reinterpret_cast<float*>(g_smem);
@@ -247,7 +258,7 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = make_float2(0.f, 0.f);
-      xv[r][s] = sT[xb[r] + slot[s]];
+      xv[r][s] = load_x<float, kXg>(sT, xb[r], slot[s], xg, cs);
     }
   }
   for (int p = 0; p < n_run; ++p) {
@@ -327,9 +338,10 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 }
 
 // One path, element loop not unrolled (large Q); accumulates per element.
-template <typename T, int Q, int R, int NT>
+template <typename T, int Q, int R, int NT, bool kXg>
 __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E, const T* __restrict__ tab,
-                                              const int (&xb)[R], const int (&ab)[R]) {
+                                              const int (&xb)[R], const int (&ab)[R], const T* __restrict__ xg,
+                                              int64_t cs) {
   constexpr int QP = QP_<Q>::v;
   T* const sT = reinterpret_cast<T*>(g_smem);
   T P[R][Q];
@@ -351,7 +363,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
     lds_vec(rho, tab + NT * QP + s * NT * QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool o = one_fraction(sT[xb[r] + rec.z], rec);
+      const bool o = one_fraction(load_x<T, kXg>(sT, xb[r], rec.z, xg, cs), rec);
       om[r] |= (uint32_t)o << s;
       if (!o) {
 #pragma unroll
@@ -785,9 +797,10 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
 // Small Q: all R rows of the lane at once (shared table loads, R-way ILP).
 // Larger Q: the lane's rows one after the other, which bounds the register
 // footprint of the whole kernel by the small-Q instantiations.
-template <typename T, int R, bool kInter, int NT>
+template <typename T, int R, bool kInter, int NT, bool kXg>
 __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E0, const T* __restrict__ table,
-                                             const T* __restrict__ gauss, const int (&xb)[R], const int (&ab)[R]) {
+                                             const T* __restrict__ gauss, const int (&xb)[R], const int (&ab)[R],
+                                             const T* __restrict__ xg, int64_t cs) {
   const int k = ph.x & 0xff, n_run = ph.x >> 16, q = ph.y;
   const int4* E = E0 + ph.z;
   const T* tab = table + ph.w;
@@ -795,8 +808,9 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
   if constexpr (!kInter && GTS_X2 && sizeof(T) == 4 && R <= 2) {
     // fp32: paired-node FFMA2 runs (Q >= 2); Q = 1 has nothing to pair
     switch (q) {
-      case 1: shap_run<T, 1, R, NT>(k, n_run, E, tab, xb, ab); break;
-#define GTS_RUN(QQ) case QQ: shap_run_x2<QQ, R, NT>(k, n_run, E, reinterpret_cast<const float*>(tab), xb, ab); break;
+      case 1: shap_run<T, 1, R, NT, kXg>(k, n_run, E, tab, xb, ab, xg, cs); break;
+#define GTS_RUN(QQ) case QQ: shap_run_x2<QQ, R, NT, kXg>(k, n_run, E, reinterpret_cast<const float*>(tab), xb, ab, \
+                                                         reinterpret_cast<const float*>(xg), cs); break;
       GTS_RUN(2) GTS_RUN(3) GTS_RUN(4)
 #if GTS_X2_R2_QMAX >= 5
       GTS_RUN(5)
@@ -810,13 +824,14 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
         for (int r = 0; r < R; ++r) {
           const int xb1[1] = {xb[r]}, ab1[1] = {ab[r]};
           switch (q) {
-#define GTS_RUN1(QQ) case QQ: shap_run_x2<QQ, 1, NT>(k, n_run, E, reinterpret_cast<const float*>(tab), xb1, ab1); break;
+#define GTS_RUN1(QQ) case QQ: shap_run_x2<QQ, 1, NT, kXg>(k, n_run, E, reinterpret_cast<const float*>(tab), xb1, ab1, \
+                                                           reinterpret_cast<const float*>(xg), cs); break;
             GTS_RUN1(5) GTS_RUN1(6) GTS_RUN1(7) GTS_RUN1(8)
 #undef GTS_RUN1
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
-#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1, NT>(k, E + p * k, tab + p * words, xb1, ab1); break;
+#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1, NT, kXg>(k, E + p * k, tab + p * words, xb1, ab1, xg, cs); break;
                   GTS_DYN(9) GTS_DYN(10) GTS_DYN(11) GTS_DYN(12) GTS_DYN(13) GTS_DYN(14) GTS_DYN(15) GTS_DYN(16)
 #undef GTS_DYN
                   default: break;
@@ -827,7 +842,7 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
     }
   } else if constexpr (!kInter) {
     switch (q) {
-#define GTS_RUN(QQ) case QQ: shap_run<T, QQ, R, NT>(k, n_run, E, tab, xb, ab); break;
+#define GTS_RUN(QQ) case QQ: shap_run<T, QQ, R, NT, kXg>(k, n_run, E, tab, xb, ab, xg, cs); break;
       GTS_RUN(1) GTS_RUN(2) GTS_RUN(3) GTS_RUN(4)
 #undef GTS_RUN
       default:
@@ -835,13 +850,13 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
         for (int r = 0; r < R; ++r) {
           const int xb1[1] = {xb[r]}, ab1[1] = {ab[r]};
           switch (q) {
-#define GTS_RUN1(QQ) case QQ: shap_run<T, QQ, 1, NT>(k, n_run, E, tab, xb1, ab1); break;
+#define GTS_RUN1(QQ) case QQ: shap_run<T, QQ, 1, NT, kXg>(k, n_run, E, tab, xb1, ab1, xg, cs); break;
             GTS_RUN1(5) GTS_RUN1(6) GTS_RUN1(7) GTS_RUN1(8)
 #undef GTS_RUN1
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
-#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1, NT>(k, E + p * k, tab + p * words, xb1, ab1); break;
+#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1, NT, kXg>(k, E + p * k, tab + p * words, xb1, ab1, xg, cs); break;
                   GTS_DYN(9) GTS_DYN(10) GTS_DYN(11) GTS_DYN(12) GTS_DYN(13) GTS_DYN(14) GTS_DYN(15) GTS_DYN(16)
 #undef GTS_DYN
                   default: break;
@@ -946,8 +961,16 @@ __host__ __device__ constexpr int tile_words_per_warp() {
 // the slot width S (upper triangle of S x S); SHAP tiles by the blob's widest
 // slot map (tile_w = max slots + 1, odd: lanes = rows hit distinct banks), so
 // identity maps of M features cost M + 1 words per row, not S + 1.
+#ifndef GTS_XG_MIN_S
+#define GTS_XG_MIN_S 64  // SHAP kernels with >= this many slots read X from feature-major global memory
+#endif
+// kXg kernels keep no X tile: every run reads its x values straight from a
+// feature-major copy of X (L1-resident for the rows in flight), which halves
+// the shared memory per row and lets twice the warps share an SM.
 template <bool kInter, int S>
-__host__ __device__ constexpr int x_stride(int tile_w) { return kInter ? S + 1 : tile_w; }
+__host__ __device__ constexpr bool xg_enabled() { return !kInter && S >= GTS_XG_MIN_S; }
+template <bool kInter, int S>
+__host__ __device__ constexpr int x_stride(int tile_w) { return kInter ? S + 1 : (xg_enabled<kInter, S>() ? 0 : tile_w); }
 template <bool kInter, int S>
 __host__ __device__ constexpr int acc_stride(int tile_w) { return kInter ? (acc_width<kInter>(S) | 1) : tile_w; }
 
@@ -973,7 +996,7 @@ __host__ __device__ constexpr int acc_stride(int tile_w) { return kInter ? (acc_
 #define GTS_SHAP_R64 1
 #endif
 #ifndef GTS_SHAP_W64
-#define GTS_SHAP_W64 6
+#define GTS_SHAP_W64 (GTS_XG_MIN_S <= 64 ? 8 : 6)  // no X tile (kXg): 8 warps x 2 blocks fit the phi tiles
 #endif
 #ifndef GTS_SHAP_B64
 #define GTS_SHAP_B64 2
@@ -1108,10 +1131,12 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   int xb[R], ab[R];
   int64_t row[R];
   bool ok[R];
+  constexpr bool kXg = xg_enabled<kInter, S>();
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int lr = warp * ROWS + r * 32 + lane;
-    xb[r] = o_x + lr * XS;
+    const int64_t rr = row0 + r * 32 + lane;
+    xb[r] = kXg ? (int)(rr < a.n_rows ? rr : a.n_rows - 1) : o_x + lr * XS;  // kXg: the (clamped) row
     ab[r] = o_acc + lr * AS;
     row[r] = row0 + r * 32 + lane;
     ok[r] = row[r] < a.n_rows;
@@ -1226,7 +1251,7 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
     }
     if (c.map_id != cur_map || c.group != cur_group) {
       flush();
-      if (c.map_id != cur_map) gather(c);
+      if (!kXg && c.map_id != cur_map) gather(c);
       cur_map = c.map_id;
       cur_group = c.group;
       cur_slots = c.n_slots;
@@ -1240,7 +1265,7 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
       const T* tab = reinterpret_cast<const T*>(sP + c.n_paths);
       for (int p = 0; p < c.n_paths;) {
         const int4 ph = sP[p];
-        run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S)>(ph, sE, tab, sT, xb, ab);
+        run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S), kXg>(ph, sE, tab, sT, xb, ab, X, a.col_stride);
         p += ph.x >> 16;
       }
       dirty = true;

@@ -24,6 +24,13 @@ if [ "${BENCH:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-ablation --extras none > $OUT/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 fi
+if [ "${TRAFFIC:-1}" = "1" ]; then
+  # DRAM bytes of the bench's own launch (default config, 2^18 rows): one metrics pass, not --set full
+  timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:nodal_kernel -s 1 -c 1 -o $OUT/traffic_bench python bench.py --steps 1 --warmup 1 --no-cpu-baseline \
+    --no-e2e --no-ablation --extras none > $OUT/traffic_bench.log 2>&1; echo "traffic pass rc=$?"
+  ncu -i $OUT/traffic_bench.ncu-rep --page raw --csv > $OUT/traffic_bench.raw.csv 2>/dev/null; rm -f $OUT/traffic_bench.ncu-rep
+fi
 if [ "${NCU:-1}" = "1" ]; then
   KEEP=1 OUT=$OUT NAME=ncu_covtype-large_shap WL=covtype-large ROWS=${CT_ROWS:-2048} MODE=shap BARGS="--rows-per-step 0 --extras none" bash scripts/ncu_one.sh
   OUT=$OUT NAME=ncu_fashion_mnist-med_shap WL=fashion_mnist-med ROWS=65536 MODE=shap BARGS="--rows-per-step 0 --extras none" bash scripts/ncu_one.sh
