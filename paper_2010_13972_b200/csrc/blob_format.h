@@ -20,8 +20,9 @@ constexpr int kQMax = 16;                 // Gauss nodes for merged k <= 31 (k =
 constexpr int kMaxChunkPaths = 256;
 constexpr int kChunkBytes = 16 * 1024;    // NODAL: staged bytes per chunk (one TMA bulk copy)
 #ifndef GTS_CHUNK_BYTES_WIDE
-#define GTS_CHUNK_BYTES_WIDE (8 * 1024)  // SHAP-only blobs with identity maps of > 16 features (r02b: 8 KB
-                                         // staging lets two blocks share an SM: covtype 9.56e3 vs 5.79e3 rows/s)
+#define GTS_CHUNK_BYTES_WIDE (16 * 1024)  // SHAP-only blobs with identity maps of > 16 features (r02b: 8 KB
+                                          // staging let two blocks share an SM while the X tile was in shared
+                                          // memory; without it (r02f) 16 KB is +2 % on covtype)
 #endif
 
 struct BlobHeader {            // 256 bytes at offset 0
@@ -52,7 +53,8 @@ static_assert(sizeof(BlobHeader) == 256, "header size");
 // NODAL: a chunk = consecutive paths of one group that touch at most max_slots
 // distinct features; a warp walks all of a chunk's paths for its rows.  Its
 // staged region (copied to shared memory with one TMA bulk copy) is
-//   int4 elem[n_elems]  {lower bits, upper bits, slot, tri-row base of slot}
+//   int4 elem[n_elems]  {lower bits, upper bits, slot, w}: w = tri-row base of the
+//                       slot (interaction tables, NT = 3) or the feature (NT = 2)
 //   int4 path[n_paths]  {k | run length << 16, Q, first elem, first table word}
 //   T    table[table_words]   (per path, see below)
 struct ChunkRec {              // 64 bytes

@@ -1005,7 +1005,9 @@ static void write_region(const PathTable& tab, const NodalPlan& np, const GaussT
       std::memcpy(&rec[0], &tab.lower[e0 + s], 4);
       std::memcpy(&rec[1], &tab.upper[e0 + s], 4);
       rec[2] = sl[s];
-      rec[3] = sl[s] * (2 * S - sl[s] - 1) / 2;  // upper-triangle row base of the slot
+      // interaction tables (nt = 3): upper-triangle row base of the slot; SHAP-only
+      // tables (nt = 2): the feature itself (kernels that read X from global memory)
+      rec[3] = nt == 3 ? sl[s] * (2 * S - sl[s] - 1) / 2 : tab.feature[e0 + s];
     }
     const double* z = &tab.zero_fraction[e0];
     const double v = tab.v[pr.src];

@@ -144,11 +144,13 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
   for (int r = 0; r < R; ++r) ph0[r] = (T)0;
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
-    slot[s] = (s < KM - 1 || s < k) ? E[s].z : 0;
+    const bool valid = (s < KM - 1 || s < k);
+    slot[s] = valid ? E[s].z : 0;
+    const int fx = kXg ? (valid ? E[s].w : 0) : slot[s];  // kXg: X is indexed by feature
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = (T)0;
-      xv[r][s] = load_x<T, kXg>(sT, xb[r], slot[s], xg, cs);
+      xv[r][s] = load_x<T, kXg>(sT, xb[r], fx, xg, cs);
     }
   }
   for (int p = 0; p < n_run; ++p) {
@@ -254,11 +256,13 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
   for (int r = 0; r < R; ++r) ph0[r] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
-    slot[s] = (s < KM - 1 || s < k) ? E[s].z : 0;
+    const bool valid = (s < KM - 1 || s < k);
+    slot[s] = valid ? E[s].z : 0;
+    const int fx = kXg ? (valid ? E[s].w : 0) : slot[s];  // kXg: X is indexed by feature
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = make_float2(0.f, 0.f);
-      xv[r][s] = load_x<float, kXg>(sT, xb[r], slot[s], xg, cs);
+      xv[r][s] = load_x<float, kXg>(sT, xb[r], fx, xg, cs);
     }
   }
   for (int p = 0; p < n_run; ++p) {
@@ -363,7 +367,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
     lds_vec(rho, tab + NT * QP + s * NT * QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool o = one_fraction(load_x<T, kXg>(sT, xb[r], rec.z, xg, cs), rec);
+      const bool o = one_fraction(load_x<T, kXg>(sT, xb[r], kXg ? rec.w : rec.z, xg, cs), rec);
       om[r] |= (uint32_t)o << s;
       if (!o) {
 #pragma unroll
@@ -962,7 +966,9 @@ __host__ __device__ constexpr int tile_words_per_warp() {
 // slot map (tile_w = max slots + 1, odd: lanes = rows hit distinct banks), so
 // identity maps of M features cost M + 1 words per row, not S + 1.
 #ifndef GTS_XG_MIN_S
-#define GTS_XG_MIN_S 64  // SHAP kernels with >= this many slots read X from feature-major global memory
+#define GTS_XG_MIN_S 32  // SHAP kernels with >= this many slots read X from feature-major global memory
+                         // (measured, profiles/r02f: fashion 5.06e5 -> 6.17e5 rows/s, the per-chunk X
+                         // gathers are gone; covtype neutral at 16 warps / SM vs 12 with the X tile)
 #endif
 // kXg kernels keep no X tile: every run reads its x values straight from a
 // feature-major copy of X (L1-resident for the rows in flight), which halves
