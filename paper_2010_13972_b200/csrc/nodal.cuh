@@ -40,6 +40,9 @@
                                                 // Q = 3 (pair + scalar tail) -4 %, padded to 4 nodes -14 %
                                                 // (profiles/r01n, r01i)
 #endif
+#ifndef GTS_INTER_CACHEU_QMAX
+#define GTS_INTER_CACHEU_QMAX 4  // interaction runs up to this Q keep u_sq of every element in registers
+#endif
 #ifndef GTS_INTER_REGACC
 #define GTS_INTER_REGACC 0  // bit Q: interaction runs with Q nodes keep the run's pair cells in registers
 #endif
@@ -523,7 +526,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
     }
     // u_s = (o_s - z_s)/f_s(t_q): cached in registers for small paths; for
     // larger ones the partner's u is applied as a select on the dot product
-    constexpr bool kCacheU = Q <= 4;  // Q = 5 would put u in local memory
+    constexpr bool kCacheU = Q <= GTS_INTER_CACHEU_QMAX;  // u of every element in registers
     T u[R][kCacheU ? KM : 1][Q];
     if constexpr (kCacheU) {
 #pragma unroll
@@ -967,8 +970,8 @@ __host__ __device__ constexpr int tile_words_per_warp() {
 // identity maps of M features cost M + 1 words per row, not S + 1.
 #ifndef GTS_XG_MIN_S
 #define GTS_XG_MIN_S 32  // SHAP kernels with >= this many slots read X from feature-major global memory
-                         // (measured, profiles/r02f: fashion 5.06e5 -> 6.17e5 rows/s, the per-chunk X
-                         // gathers are gone; covtype neutral at 16 warps / SM vs 12 with the X tile)
+                         // (measured, profiles/r02f-g: with 2 rows per lane fashion 5.06e5 -> 6.14e5 rows/s,
+                         // the per-chunk X gathers are gone; covtype 1.40e4 -> 1.43e4)
 #endif
 // kXg kernels keep no X tile: every run reads its x values straight from a
 // feature-major copy of X (L1-resident for the rows in flight), which halves
@@ -990,19 +993,19 @@ __host__ __device__ constexpr int acc_stride(int tile_w) { return kInter ? (acc_
 #define GTS_INTER8_MINB 2  // resident blocks per SM the 8-slot fp32 interaction kernel's registers are sized for
 #endif
 #ifndef GTS_SHAP_R32
-#define GTS_SHAP_R32 1  // measured (profiles/r02b): R 1 / W 8 3.02e5 rows/s fashion, R 2 / W 4 2.49e5
+#define GTS_SHAP_R32 2  // measured with global X (profiles/r02g): fashion R 2 / W 4 6.14e5 rows/s, R 1 / W 8 4.44e5
 #endif
 #ifndef GTS_SHAP_W32
-#define GTS_SHAP_W32 8
+#define GTS_SHAP_W32 4
 #endif
 #ifndef GTS_SHAP_B32
 #define GTS_SHAP_B32 2  // resident blocks per SM the register budget is sized for
 #endif
 #ifndef GTS_SHAP_R64
-#define GTS_SHAP_R64 1
+#define GTS_SHAP_R64 2  // measured with global X (profiles/r02g): covtype R 2 / W 4 1.43e4 rows/s, R 1 / W 8 1.38e4
 #endif
 #ifndef GTS_SHAP_W64
-#define GTS_SHAP_W64 (GTS_XG_MIN_S <= 64 ? 8 : 6)  // no X tile (kXg): 8 warps x 2 blocks fit the phi tiles
+#define GTS_SHAP_W64 4  // no X tile (kXg): 4 warps x 64 rows x 2 blocks fit the phi tiles
 #endif
 #ifndef GTS_SHAP_B64
 #define GTS_SHAP_B64 2
