@@ -238,10 +238,11 @@ gts_status gts_blob_write_range(const gts_bins* bins, const gts_blob_info* info,
    d_phi:   device [n_rows][n_groups][n_features+1] of info->dtype, fully
             overwritten; column n_features holds the bias phi_0 (reading G14).
    stream:  cudaStream_t (NULL = default stream).  n_rows == 0 is a no-op.
-   Temporary device memory: for NODAL blobs of 64 slots the kernel reads X
-   feature-major, so a row-major X is first transposed into a stream-ordered
-   allocation of n_rows * n_features elements (cudaMallocAsync, freed after
-   the kernel on the same stream; OUT_OF_MEMORY if it fails).               */
+   Temporary device memory: for NODAL blobs of 32 or 64 slots the kernel
+   reads X feature-major, so X is first copied (transposed if row-major) into
+   a stream-ordered allocation of about n_rows * n_features elements, padded
+   to whole row tiles (cudaMallocAsync, freed after the kernel on the same
+   stream; OUT_OF_MEMORY if it fails).                                      */
 gts_status gts_shap(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows,
                     int64_t ld_x, void* d_phi, void* stream);
 
@@ -296,9 +297,8 @@ gts_status gts_validate_x(gts_dtype dtype, const void* d_X, int64_t n_rows, int3
    with per-chunk slot maps (n_features > max_slots) add one pass to the
    interaction calls: the kernel adds each pair to (i, j), i < j, only, and a
    tiled transpose copies it to (j, i) (phi_ij is symmetric, Eq. 3).  NODAL
-   SHAP blobs of 64 slots add one X transpose to gts_shap (row-major X: the
-   kernel reads a feature-major copy; feature-major X through gts_shap_strided
-   skips it, so for those calls the count is one high). */
+   SHAP blobs of 32 or 64 slots add one X copy kernel to gts_shap (the kernel
+   reads a padded feature-major copy of X). */
 int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions);
 
 const char* gts_last_error(void);

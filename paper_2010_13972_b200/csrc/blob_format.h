@@ -53,8 +53,9 @@ static_assert(sizeof(BlobHeader) == 256, "header size");
 // NODAL: a chunk = consecutive paths of one group that touch at most max_slots
 // distinct features; a warp walks all of a chunk's paths for its rows.  Its
 // staged region (copied to shared memory with one TMA bulk copy) is
-//   int4 elem[n_elems]  {lower bits, upper bits, slot, w}: w = tri-row base of the
-//                       slot (interaction tables, NT = 3) or the feature (NT = 2)
+//   int4 elem[n_elems]  {lower bits, upper bits, slot, w}: NT = 3 (interaction
+//                       tables): slot index, tri-row base of the slot; NT = 2
+//                       (SHAP only): slot byte offset (slot * sizeof(T)), feature
 //   int4 path[n_paths]  {k | run length << 16, Q, first elem, first table word}
 //   T    table[table_words]   (per path, see below)
 struct ChunkRec {              // 64 bytes

@@ -1004,9 +1004,10 @@ static void write_region(const PathTable& tab, const NodalPlan& np, const GaussT
       int32_t* rec = E + 4 * (int64_t)(pr.elem + s);
       std::memcpy(&rec[0], &tab.lower[e0 + s], 4);
       std::memcpy(&rec[1], &tab.upper[e0 + s], 4);
-      rec[2] = sl[s];
-      // interaction tables (nt = 3): upper-triangle row base of the slot; SHAP-only
-      // tables (nt = 2): the feature itself (kernels that read X from global memory)
+      // interaction tables (nt = 3): the slot and the upper-triangle row base of
+      // the slot; SHAP-only tables (nt = 2): the slot's byte offset in a tile row
+      // and the feature itself (kernels that read X from global memory)
+      rec[2] = nt == 3 ? sl[s] : sl[s] * (int32_t)sizeof(T);
       rec[3] = nt == 3 ? sl[s] * (2 * S - sl[s] - 1) / 2 : tab.feature[e0 + s];
     }
     const double* z = &tab.zero_fraction[e0];

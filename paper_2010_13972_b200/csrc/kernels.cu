@@ -133,11 +133,13 @@ __global__ void nonfinite_kernel(const T* __restrict__ X, int64_t n_rows, int M,
   }
 }
 
-// Feature-major copy of row-major X (xt[f * n + r] = X[r * rs + f]) for the
-// kernels that read X from global memory (nodal::xg_enabled): 32 x 32 tiles
-// through shared memory, coalesced on both sides.
+// Feature-major copy of X for the kernels that read X from global memory
+// (nodal::xg_enabled): xt[f * ld + r] = X[r][f] for r < n.  Row-major X goes
+// through 32 x 32 shared tiles (coalesced on both sides); feature-major X is a
+// strided column copy.
 template <typename T>
-__global__ void transpose_x_kernel(const T* __restrict__ X, int64_t n, int M, int64_t rs, T* __restrict__ xt) {
+__global__ void transpose_x_kernel(const T* __restrict__ X, int64_t n, int M, int64_t rs, T* __restrict__ xt,
+                                   int64_t ld) {
   __shared__ T tile[32][33];
   const int64_t tiles_r = (n + 31) / 32;
   const int tiles_f = (M + 31) / 32;
@@ -153,9 +155,19 @@ __global__ void transpose_x_kernel(const T* __restrict__ X, int64_t n, int M, in
     for (int y = threadIdx.y; y < 32; y += blockDim.y) {
       const int f = f0 + y;
       const int64_t r = r0 + threadIdx.x;
-      if (r < n && f < M) xt[(int64_t)f * n + r] = tile[threadIdx.x][y];
+      if (r < n && f < M) xt[(int64_t)f * ld + r] = tile[threadIdx.x][y];
     }
     __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void copy_cols_kernel(const T* __restrict__ X, int64_t n, int M, int64_t cs, T* __restrict__ xt,
+                                 int64_t ld) {
+  const int64_t total = n * M;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = i / n, r = i - f * n;
+    xt[f * ld + r] = X[f * cs + r];
   }
 }
 
@@ -215,25 +227,50 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   auto kern = nodal::nodal_kernel<T, S, W, R, kInter>;
   const size_t smem = nodal_smem_bytes<T, kInter, S>(info);
   if (smem > 227 * 1024) return fail(GTS_ERR_INVALID_ARGUMENT, "chunk staging needs %zu bytes of shared memory", smem);
-  void* xt = nullptr;  // feature-major scratch copy of a row-major X (xg kernels)
-  if (nodal::xg_enabled<kInter, S>() && rs != 1 && info->n_units > 0) {
-    const size_t bytes = (size_t)n_rows * info->n_features * sizeof(T);
-    if (cudaMallocAsync(&xt, bytes, st) != cudaSuccess)
-      return fail(GTS_ERR_OUT_OF_MEMORY, "cudaMallocAsync of %zu bytes for the feature-major X copy failed", bytes);
-    const int64_t tiles = ((n_rows + 31) / 32) * ((info->n_features + 31) / 32);
-    const int tb = (int)std::min<int64_t>(tiles, (int64_t)num_sms() * 16);
-    transpose_x_kernel<T><<<tb, dim3(32, 8), 0, st>>>(static_cast<const T*>(d_X), n_rows, info->n_features, rs,
-                                                       static_cast<T*>(xt));
-    gts_status s0 = cuda_check("X transpose launch");
-    if (s0 != GTS_OK) {
-      cudaFreeAsync(xt, st);
-      return s0;
+  void* xt = nullptr;  // padded feature-major scratch copy of X (xg kernels)
+  if constexpr (nodal::xg_enabled<kInter, S>()) {
+    if (info->n_units > 0) {
+      const int M = info->n_features;
+      const int64_t rpb = (int64_t)W * 32 * R;
+      // element indices feature * ld + row are 32-bit in the kernel: split huge calls
+      const int64_t max_rows = std::max<int64_t>(rpb, ((INT32_MAX / std::max(M, 1)) / rpb - 1) * rpb);
+      if (n_rows > max_rows) {
+        const int64_t out_row = (int64_t)info->n_groups * (info->n_features + 1);
+        for (int64_t r0 = 0; r0 < n_rows; r0 += max_rows) {
+          const T* xs = static_cast<const T*>(d_X) + r0 * rs;
+          T* os = static_cast<T*>(out) + r0 * out_row;
+          gts_status s0 = launch_nodal<T, kInter, S>(info, d_blob, xs, std::min(max_rows, n_rows - r0), rs, cs, os, st,
+                                                     out_phi);
+          if (s0 != GTS_OK) return s0;
+        }
+        return GTS_OK;
+      }
+      const int64_t ld = (n_rows + rpb - 1) / rpb * rpb;  // whole row tiles: lanes of the last tile read the pad
+      const size_t bytes = (size_t)ld * M * sizeof(T);
+      if (cudaMallocAsync(&xt, bytes, st) != cudaSuccess)
+        return fail(GTS_ERR_OUT_OF_MEMORY, "cudaMallocAsync of %zu bytes for the feature-major X copy failed", bytes);
+      if (ld > n_rows)
+        cudaMemset2DAsync(static_cast<T*>(xt) + n_rows, (size_t)ld * sizeof(T), 0, (size_t)(ld - n_rows) * sizeof(T),
+                          (size_t)M, st);
+      if (rs == 1 && cs != 1) {  // feature-major input
+        const int blocks = (int)std::min<int64_t>((n_rows * M + 255) / 256, (int64_t)num_sms() * 16);
+        copy_cols_kernel<T><<<blocks, 256, 0, st>>>(static_cast<const T*>(d_X), n_rows, M, cs, static_cast<T*>(xt), ld);
+      } else {
+        const int64_t tiles = ((n_rows + 31) / 32) * ((M + 31) / 32);
+        const int tb = (int)std::min<int64_t>(tiles, (int64_t)num_sms() * 16);
+        transpose_x_kernel<T><<<tb, dim3(32, 8), 0, st>>>(static_cast<const T*>(d_X), n_rows, M, rs,
+                                                           static_cast<T*>(xt), ld);
+      }
+      gts_status s0 = cuda_check("X transpose launch");
+      if (s0 != GTS_OK) {
+        cudaFreeAsync(xt, st);
+        return s0;
+      }
+      d_X = xt;
+      rs = 1;
+      cs = ld;
     }
-    d_X = xt;
-    rs = 1;
-    cs = n_rows;
   }
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   per_sm = std::max(per_sm, 1);

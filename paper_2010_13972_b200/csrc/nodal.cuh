@@ -43,6 +43,9 @@
 #ifndef GTS_INTER_CACHEU_QMAX
 #define GTS_INTER_CACHEU_QMAX 4  // interaction runs up to this Q keep u_sq of every element in registers
 #endif
+#ifndef GTS_INTER_X2_PATH
+#define GTS_INTER_X2_PATH 0  // bit Q: fp32 interaction paths with Q nodes on paired Gauss nodes (inter_path_x2)
+#endif
 #ifndef GTS_INTER_REGACC
 #define GTS_INTER_REGACC 0  // bit Q: interaction runs with Q nodes keep the run's pair cells in registers
 #endif
@@ -116,14 +119,25 @@ __device__ __forceinline__ bool one_fraction(T x, int4 rec) {
   return (x >= (T)__int_as_float(rec.x)) & (x < (T)__int_as_float(rec.y));
 }
 
-// x value of lane-row xb at a slot: from the warp's shared X tile (xb = tile
-// row base), or, for kXg kernels, straight from feature-major X in global
-// memory (xb = the row; consecutive lanes read consecutive rows of one
-// feature: one coalesced, L1-resident line per warp instruction).
-template <typename T, bool kXg>
-__device__ __forceinline__ T load_x(const T* sT, int xb, int slot, const T* __restrict__ xg, int64_t cs) {
-  if constexpr (kXg) return __ldg(xg + (int64_t)slot * cs + xb);
-  else return sT[xb + slot];
+// x value of lane-row xb for element record rec: from the warp's shared X
+// tile (xb = tile row base, rec.z = slot), or, for kXg kernels, straight from
+// a feature-major copy of X in global memory (xb = the row, rec.w = the
+// feature; consecutive lanes read consecutive rows of one feature: one
+// coalesced, L1-resident line per warp instruction; the launcher keeps
+// feature * cs + row within 32 bits).  SHAP-only records (NT = 2) hold the
+// slot as a byte offset into a tile row.
+template <typename T, int NT, bool kXg>
+__device__ __forceinline__ T load_x(const T* sT, int xb, int4 rec, const T* __restrict__ xg, int cs) {
+  if constexpr (kXg) return __ldg(xg + (uint32_t)(rec.w * cs + xb));
+  else return sT[xb + (NT == 2 ? rec.z / (int)sizeof(T) : rec.z)];
+}
+
+// The phi tile cell of lane-row ab (word index of its tile row) at a slot
+// (NT = 2: byte offset; else word index).
+template <typename T, int NT>
+__device__ __forceinline__ T& tile_at(int ab, int slot) {
+  if constexpr (NT == 2) return *reinterpret_cast<T*>(g_smem + ab * (int)sizeof(T) + slot);
+  else return reinterpret_cast<T*>(g_smem)[ab + slot];
 }
 
 // --------------------------------------------------------------------- SHAP
@@ -136,7 +150,7 @@ __device__ __forceinline__ T load_x(const T* sT, int xb, int slot, const T* __re
 // path into one register per row and added to every slot of the run at its end.
 template <typename T, int Q, int R, int NT, bool kXg>
 __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restrict__ E, const T* __restrict__ tab,
-                                         const int (&xb)[R], const int (&ab)[R], const T* __restrict__ xg, int64_t cs) {
+                                         const int (&xb)[R], const int (&ab)[R], const T* __restrict__ xg, int cs) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q;
   constexpr int kRmw = GTS_RMW_REGS / R > 1 ? GTS_RMW_REGS / R : 1;
   T* const sT = reinterpret_cast<T*>(g_smem);
@@ -148,12 +162,13 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
     const bool valid = (s < KM - 1 || s < k);
-    slot[s] = valid ? E[s].z : 0;
-    const int fx = kXg ? (valid ? E[s].w : 0) : slot[s];  // kXg: X is indexed by feature
+    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
+    slot[s] = e.z;
+    const T* px = xg + (uint32_t)(e.w * cs + xb[0]);  // kXg: the lane's R rows are 32 apart
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = (T)0;
-      xv[r][s] = load_x<T, kXg>(sT, xb[r], fx, xg, cs);
+      xv[r][s] = kXg ? __ldg(px + r * 32) : load_x<T, NT, false>(sT, xb[r], e, xg, cs);
     }
   }
   for (int p = 0; p < n_run; ++p) {
@@ -226,14 +241,14 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
       const int s = s0 + b;
       if (s < KM && (s < KM - 1 || s < k))
 #pragma unroll
-        for (int r = 0; r < R; ++r) old[r][b] = sT[ab[r] + slot[s]];
+        for (int r = 0; r < R; ++r) old[r][b] = tile_at<T, NT>(ab[r], slot[s]);
     }
 #pragma unroll
     for (int b = 0; b < kRmw; ++b) {
       const int s = s0 + b;
       if (s < KM && (s < KM - 1 || s < k))
 #pragma unroll
-        for (int r = 0; r < R; ++r) sT[ab[r] + slot[s]] = old[r][b] + (acc[r][s] + ph0[r]);
+        for (int r = 0; r < R; ++r) tile_at<T, NT>(ab[r], slot[s]) = old[r][b] + (acc[r][s] + ph0[r]);
     }
   }
 }
@@ -247,7 +262,7 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 template <int Q, int R, int NT, bool kXg>
 __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __restrict__ E,
                                             const float* __restrict__ tab, const int (&xb)[R], const int (&ab)[R],
-                                            const float* __restrict__ xg, int64_t cs) {
+                                            const float* __restrict__ xg, int cs) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q, QH = (Q + 1) / 2;
   constexpr int kRmw = GTS_RMW_REGS / R > 1 ? GTS_RMW_REGS / R : 1;
   float* const sT = reinterpret_cast<float*>(g_smem);
@@ -260,12 +275,13 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
     const bool valid = (s < KM - 1 || s < k);
-    slot[s] = valid ? E[s].z : 0;
-    const int fx = kXg ? (valid ? E[s].w : 0) : slot[s];  // kXg: X is indexed by feature
+    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
+    slot[s] = e.z;
+    const float* px = xg + (uint32_t)(e.w * cs + xb[0]);  // kXg: the lane's R rows are 32 apart
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = make_float2(0.f, 0.f);
-      xv[r][s] = load_x<float, kXg>(sT, xb[r], fx, xg, cs);
+      xv[r][s] = kXg ? __ldg(px + r * 32) : load_x<float, NT, false>(sT, xb[r], e, xg, cs);
     }
   }
   for (int p = 0; p < n_run; ++p) {
@@ -331,7 +347,7 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
       const int s = s0 + b;
       if (s < KM && (s < KM - 1 || s < k))
 #pragma unroll
-        for (int r = 0; r < R; ++r) old[r][b] = sT[ab[r] + slot[s]];
+        for (int r = 0; r < R; ++r) old[r][b] = tile_at<float, NT>(ab[r], slot[s]);
     }
 #pragma unroll
     for (int b = 0; b < kRmw; ++b) {
@@ -339,7 +355,7 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
       if (s < KM && (s < KM - 1 || s < k))
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          sT[ab[r] + slot[s]] = old[r][b] + ((acc[r][s].x + acc[r][s].y) + (ph0[r].x + ph0[r].y));
+          tile_at<float, NT>(ab[r], slot[s]) = old[r][b] + ((acc[r][s].x + acc[r][s].y) + (ph0[r].x + ph0[r].y));
     }
   }
 }
@@ -348,7 +364,7 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 template <typename T, int Q, int R, int NT, bool kXg>
 __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E, const T* __restrict__ tab,
                                               const int (&xb)[R], const int (&ab)[R], const T* __restrict__ xg,
-                                              int64_t cs) {
+                                              int cs) {
   constexpr int QP = QP_<Q>::v;
   T* const sT = reinterpret_cast<T*>(g_smem);
   T P[R][Q];
@@ -370,7 +386,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
     lds_vec(rho, tab + NT * QP + s * NT * QP);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool o = one_fraction(load_x<T, kXg>(sT, xb[r], kXg ? rec.w : rec.z, xg, cs), rec);
+      const bool o = one_fraction(load_x<T, NT, kXg>(sT, xb[r], rec, xg, cs), rec);
       om[r] |= (uint32_t)o << s;
       if (!o) {
 #pragma unroll
@@ -402,7 +418,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
 #pragma unroll
         for (int q = 0; q < Q; ++q) a = fma(P[r][q], C[q], a);
       }
-      sT[ab[r] + sl] += a;
+      tile_at<T, NT>(ab[r], sl) += a;
     }
   }
 }
@@ -799,6 +815,66 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
   }
 }
 
+// fp32, one row: inter_path on packed pairs of Gauss nodes (FMUL2 / FFMA2);
+// the pad node of odd Q has zero tables (c = h = alpha = gamma = 0), so it
+// contributes nothing.  Pair cells are accumulated straight into the tile.
+template <int Q>
+__device__ __forceinline__ void inter_path_x2(int k, const int4* __restrict__ E, const float* __restrict__ tp,
+                                              const float* __restrict__ gam, const int (&xb)[1], const int (&ab)[1]) {
+  constexpr int QP = QP_<Q>::v, QH = (Q + 1) / 2;
+  float* const sT = reinterpret_cast<float*>(g_smem);
+  float2 G[QH], P[QH], W[QH];
+#pragma unroll
+  for (int h = 0; h < QH; ++h) G[h] = make_float2(gam[2 * h], gam[2 * h + 1]);
+  lds_pairs(P, tp);
+  uint32_t om = 0u;
+#pragma unroll 1
+  for (int s = 0; s < k; ++s) {
+    const int4 rec = E[s];
+    const bool o = one_fraction(sT[xb[0] + rec.z], rec);
+    om |= (uint32_t)o << s;
+    if (!o) {
+      float2 rh[QH];
+      lds_pairs(rh, tp + 3 * QP + s * 3 * QP);
+#pragma unroll
+      for (int h = 0; h < QH; ++h) P[h] = __fmul2_rn(P[h], rh[h]);  // EXTEND
+    }
+  }
+  {
+    float2 hh[QH];
+    lds_pairs(hh, tp + 2 * QP);
+#pragma unroll
+    for (int h = 0; h < QH; ++h) W[h] = __fmul2_rn(P[h], hh[h]);  // W_q = h_q P_q
+  }
+#pragma unroll 1
+  for (int i = 0; i < k; ++i) {
+    const int4 ri = E[i];
+    float2 ai[QH], y[QH];
+    lds_pairs(ai, tp + 3 * QP + i * 3 * QP + 2 * QP);
+    const bool oi = (om >> i) & 1u;
+    float2 ph = make_float2(0.f, 0.f), g = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int h = 0; h < QH; ++h) {
+      const float2 u = oi ? ai[h] : G[h];  // UNWIND(i) folded into u
+      y[h] = __fmul2_rn(W[h], u);
+      ph = __ffma2_rn(y[h], make_float2(2.f, 2.f), ph);  // phi_i = 2 sum_q W_q u_iq
+      g = __ffma2_rn(y[h], G[h], g);
+    }
+    sT[ab[0] + ri.w + ri.z] += ph.x + ph.y;  // Eq. 6 applied at flush
+    const float yg = g.x + g.y;
+#pragma unroll 1
+    for (int j = i + 1; j < k; ++j) {
+      const int cell = ri.w + E[j].z;
+      float2 aj[QH];
+      lds_pairs(aj, tp + 3 * QP + j * 3 * QP + 2 * QP);
+      float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int h = 0; h < QH; ++h) s2 = __ffma2_rn(y[h], aj[h], s2);
+      sT[ab[0] + cell] += ((om >> j) & 1u) ? (s2.x + s2.y) : yg;
+    }
+  }
+}
+
 // ------------------------------------------------------------- dispatch
 
 // Small Q: all R rows of the lane at once (shared table loads, R-way ILP).
@@ -807,7 +883,7 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
 template <typename T, int R, bool kInter, int NT, bool kXg>
 __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E0, const T* __restrict__ table,
                                              const T* __restrict__ gauss, const int (&xb)[R], const int (&ab)[R],
-                                             const T* __restrict__ xg, int64_t cs) {
+                                             const T* __restrict__ xg, int cs) {
   const int k = ph.x & 0xff, n_run = ph.x >> 16, q = ph.y;
   const int4* E = E0 + ph.z;
   const T* tab = table + ph.w;
@@ -905,19 +981,47 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
                 inter_run<T, 4, 1, false>(k, n_run, E, tab, gam, xb1, ab1);
               }
               break;
-            case 5: inter_run<T, 5, 1, (GTS_INTER_REGACC & (1 << 5)) != 0>(k, n_run, E, tab, gam, xb1, ab1); break;
+            case 5:
+              if constexpr (sizeof(T) == 4 && (GTS_INTER_X2_PATH & (1 << 5))) {
+                for (int p = 0; p < n_run; ++p)
+                  inter_path_x2<5>(k, E + p * k, reinterpret_cast<const float*>(tab) + p * words,
+                                   reinterpret_cast<const float*>(gam), xb1, ab1);
+              } else {
+                inter_run<T, 5, 1, (GTS_INTER_REGACC & (1 << 5)) != 0>(k, n_run, E, tab, gam, xb1, ab1);
+              }
+              break;
             case 6:
-              if constexpr (sizeof(T) == 4) {
+              if constexpr (sizeof(T) == 4 && (GTS_INTER_X2_PATH & (1 << 6))) {
+                for (int p = 0; p < n_run; ++p)
+                  inter_path_x2<6>(k, E + p * k, reinterpret_cast<const float*>(tab) + p * words,
+                                   reinterpret_cast<const float*>(gam), xb1, ab1);
+                break;
+              } else if constexpr (sizeof(T) == 4) {
                 inter_run<T, 6, 1, (GTS_INTER_REGACC & (1 << 6)) != 0>(k, n_run, E, tab, gam, xb1, ab1);
                 break;
               }
               [[fallthrough]];
             case 7:
-              if constexpr (sizeof(T) == 4) {
+              if constexpr (sizeof(T) == 4 && (GTS_INTER_X2_PATH & (1 << 7))) {
+                if (q == 7) {
+                  for (int p = 0; p < n_run; ++p)
+                    inter_path_x2<7>(k, E + p * k, reinterpret_cast<const float*>(tab) + p * words,
+                                     reinterpret_cast<const float*>(gam), xb1, ab1);
+                  break;
+                }
+              } else if constexpr (sizeof(T) == 4) {
                 if (q == 7) { inter_run<T, 7, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break; }
               }
               [[fallthrough]];
             default:
+              if constexpr (sizeof(T) == 4 && (GTS_INTER_X2_PATH & (1 << 8))) {
+                if (q == 8) {
+                  for (int p = 0; p < n_run; ++p)
+                    inter_path_x2<8>(k, E + p * k, reinterpret_cast<const float*>(tab) + p * words,
+                                     reinterpret_cast<const float*>(gam), xb1, ab1);
+                  break;
+                }
+              }
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
 #define GTS_IP(QQ) case QQ: inter_path<T, QQ, 1, false>(k, E + p * k, tab + p * words, gam, xb1, ab1); break;
@@ -981,7 +1085,10 @@ __host__ __device__ constexpr bool xg_enabled() { return !kInter && S >= GTS_XG_
 template <bool kInter, int S>
 __host__ __device__ constexpr int x_stride(int tile_w) { return kInter ? S + 1 : (xg_enabled<kInter, S>() ? 0 : tile_w); }
 template <bool kInter, int S>
-__host__ __device__ constexpr int acc_stride(int tile_w) { return kInter ? (acc_width<kInter>(S) | 1) : tile_w; }
+__host__ __device__ constexpr int acc_stride(int tile_w) {
+  // kXg kernels: a compile-time row stride S + 1 (odd), so the R rows of a lane sit at immediate offsets
+  return kInter ? (acc_width<kInter>(S) | 1) : (xg_enabled<kInter, S>() ? S + 1 : tile_w);
+}
 
 // Launch shape per (dtype, kernel, slot width): R rows per lane and W warps
 // per block.  Interactions and narrow SHAP tiles: two blocks (tiles + chunk
@@ -1145,7 +1252,7 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   for (int r = 0; r < R; ++r) {
     const int lr = warp * ROWS + r * 32 + lane;
     const int64_t rr = row0 + r * 32 + lane;
-    xb[r] = kXg ? (int)(rr < a.n_rows ? rr : a.n_rows - 1) : o_x + lr * XS;  // kXg: the (clamped) row
+    xb[r] = kXg ? (int)rr : o_x + lr * XS;  // kXg: the row (the feature-major copy is padded to whole tiles)
     ab[r] = o_acc + lr * AS;
     row[r] = row0 + r * 32 + lane;
     ok[r] = row[r] < a.n_rows;
@@ -1274,7 +1381,7 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
       const T* tab = reinterpret_cast<const T*>(sP + c.n_paths);
       for (int p = 0; p < c.n_paths;) {
         const int4 ph = sP[p];
-        run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S), kXg>(ph, sE, tab, sT, xb, ab, X, a.col_stride);
+        run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S), kXg>(ph, sE, tab, sT, xb, ab, X, (int)a.col_stride);
         p += ph.x >> 16;
       }
       dirty = true;
