@@ -271,6 +271,7 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
       cs = ld;
     }
   }
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   per_sm = std::max(per_sm, 1);
