@@ -1072,6 +1072,9 @@ __host__ __device__ constexpr int tile_words_per_warp() {
 // the slot width S (upper triangle of S x S); SHAP tiles by the blob's widest
 // slot map (tile_w = max slots + 1, odd: lanes = rows hit distinct banks), so
 // identity maps of M features cost M + 1 words per row, not S + 1.
+#ifndef GTS_XG_FIXED_STRIDE
+#define GTS_XG_FIXED_STRIDE 1  // global-X SHAP kernels: phi tile row stride S + 1 (compile time) or the blob's widest map + 1
+#endif
 #ifndef GTS_XG_MIN_S
 #define GTS_XG_MIN_S 32  // SHAP kernels with >= this many slots read X from feature-major global memory
                          // (measured, profiles/r02f-g: with 2 rows per lane fashion 5.06e5 -> 6.14e5 rows/s,
@@ -1087,7 +1090,7 @@ __host__ __device__ constexpr int x_stride(int tile_w) { return kInter ? S + 1 :
 template <bool kInter, int S>
 __host__ __device__ constexpr int acc_stride(int tile_w) {
   // kXg kernels: a compile-time row stride S + 1 (odd), so the R rows of a lane sit at immediate offsets
-  return kInter ? (acc_width<kInter>(S) | 1) : (xg_enabled<kInter, S>() ? S + 1 : tile_w);
+  return kInter ? (acc_width<kInter>(S) | 1) : (xg_enabled<kInter, S>() && GTS_XG_FIXED_STRIDE ? S + 1 : tile_w);
 }
 
 // Launch shape per (dtype, kernel, slot width): R rows per lane and W warps
