@@ -20,9 +20,8 @@ constexpr int kQMax = 16;                 // Gauss nodes for merged k <= 31 (k =
 constexpr int kMaxChunkPaths = 256;
 constexpr int kChunkBytes = 16 * 1024;    // NODAL: staged bytes per chunk (one TMA bulk copy)
 #ifndef GTS_CHUNK_BYTES_WIDE
-#define GTS_CHUNK_BYTES_WIDE (16 * 1024)  // SHAP-only blobs with identity maps of > 16 features (r02b: 8 KB
-                                          // staging let two blocks share an SM while the X tile was in shared
-                                          // memory; without it (r02f) 16 KB is +2 % on covtype)
+#define GTS_CHUNK_BYTES_WIDE (8 * 1024)  // SHAP-only blobs with identity maps of > 16 features: 8 KB staging
+                                         // lets three 4-warp blocks share an SM (covtype, profiles/r02j)
 #endif
 
 struct BlobHeader {            // 256 bytes at offset 0

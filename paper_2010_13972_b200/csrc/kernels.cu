@@ -44,32 +44,14 @@ namespace {
 
 // ------------------------------------------------------------ init kernels
 
-// phi[row][g][m] = (m == M) ? bias[g] : 0           (reading G14)
+// The outputs are zeroed with cudaMemsetAsync; this kernel then writes the
+// bias cells (reading G14): phi[row][g][M] = bias[g] (stride M + 1, cell M) or
+// phi_ij[row][g][M][M] = bias[g] (stride (M + 1)^2, cell (M + 1)^2 - 1).
 template <typename T>
-__global__ void init_phi_kernel(T* __restrict__ phi, int64_t n_rows, int G, int M,
-                                const double* __restrict__ bias) {
-  const int64_t M1 = M + 1;
-  const int64_t total = n_rows * G * M1;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i % M1;
-    const int64_t g = (i / M1) % G;
-    phi[i] = (m == M) ? (T)bias[g] : (T)0;
-  }
-}
-
-// phi_ij[row][g][a][b] = (a == M && b == M) ? bias[g] : 0
-template <typename T>
-__global__ void init_phi_ij_kernel(T* __restrict__ phi, int64_t n_rows, int G, int M,
-                                   const double* __restrict__ bias) {
-  const int64_t M1 = M + 1, MM = M1 * M1;
-  const int64_t total = n_rows * G * MM;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t cell = i % MM;
-    const int64_t g = (i / MM) % G;
-    phi[i] = (cell == MM - 1) ? (T)bias[g] : (T)0;
-  }
+__global__ void bias_cells_kernel(T* __restrict__ out, int64_t n_rg, int G, int64_t stride, int64_t cell,
+                                  const double* __restrict__ bias) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rg; i += (int64_t)gridDim.x * blockDim.x)
+    out[i * stride + cell] = (T)bias[i % G];
 }
 
 // phi_ij is symmetric (Eq. 3).  With per-chunk slot maps (wide models) the
@@ -192,17 +174,13 @@ gts_status launch_init(bool inter, const gts_blob_info* info, const char* d_blob
                        cudaStream_t st) {
   const double* bias = reinterpret_cast<const double*>(d_blob + kBiasOffset);
   const int64_t M1 = info->n_features + 1;
-  const int64_t total = n_rows * info->n_groups * (inter ? M1 * M1 : M1);
-  const int threads = 256;
-  const int64_t want = (total + threads - 1) / threads;
-  const int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * 16);
-  if (inter)
-    init_phi_ij_kernel<T><<<blocks, threads, 0, st>>>(static_cast<T*>(out), n_rows, info->n_groups,
-                                                       info->n_features, bias);
-  else
-    init_phi_kernel<T><<<blocks, threads, 0, st>>>(static_cast<T*>(out), n_rows, info->n_groups,
-                                                    info->n_features, bias);
-  return cuda_check("init kernel launch");
+  const int64_t stride = inter ? M1 * M1 : M1;
+  const int64_t n_rg = n_rows * info->n_groups;
+  if (cudaMemsetAsync(out, 0, (size_t)(n_rg * stride) * sizeof(T), st) != cudaSuccess)
+    return cuda_check("output zero fill");
+  const int blocks = (int)std::min<int64_t>((n_rg + 255) / 256, (int64_t)num_sms() * 8);
+  bias_cells_kernel<T><<<blocks, 256, 0, st>>>(static_cast<T*>(out), n_rg, info->n_groups, stride, stride - 1, bias);
+  return cuda_check("bias kernel launch");
 }
 
 size_t nodal_buffer_bytes(const gts_blob_info* info) {

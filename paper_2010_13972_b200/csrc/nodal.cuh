@@ -42,9 +42,8 @@
 #endif
 #ifndef GTS_INTER_CACHEU_QMAX
 #define GTS_INTER_CACHEU_QMAX 4  // interaction runs up to this Q keep u_sq of every element in registers
-#endif
-#ifndef GTS_INTER_X2_PATH
-#define GTS_INTER_X2_PATH 0  // bit Q: fp32 interaction paths with Q nodes on paired Gauss nodes (inter_path_x2)
+                                 // (measured, profiles/r02h: 5, 6, 7 cost adult 12-16 %; a paired-node
+                                 // per-path variant for Q >= 5 cost 28 %, r02j)
 #endif
 #ifndef GTS_INTER_REGACC
 #define GTS_INTER_REGACC 0  // bit Q: interaction runs with Q nodes keep the run's pair cells in registers
@@ -815,66 +814,6 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
   }
 }
 
-// fp32, one row: inter_path on packed pairs of Gauss nodes (FMUL2 / FFMA2);
-// the pad node of odd Q has zero tables (c = h = alpha = gamma = 0), so it
-// contributes nothing.  Pair cells are accumulated straight into the tile.
-template <int Q>
-__device__ __forceinline__ void inter_path_x2(int k, const int4* __restrict__ E, const float* __restrict__ tp,
-                                              const float* __restrict__ gam, const int (&xb)[1], const int (&ab)[1]) {
-  constexpr int QP = QP_<Q>::v, QH = (Q + 1) / 2;
-  float* const sT = reinterpret_cast<float*>(g_smem);
-  float2 G[QH], P[QH], W[QH];
-#pragma unroll
-  for (int h = 0; h < QH; ++h) G[h] = make_float2(gam[2 * h], gam[2 * h + 1]);
-  lds_pairs(P, tp);
-  uint32_t om = 0u;
-#pragma unroll 1
-  for (int s = 0; s < k; ++s) {
-    const int4 rec = E[s];
-    const bool o = one_fraction(sT[xb[0] + rec.z], rec);
-    om |= (uint32_t)o << s;
-    if (!o) {
-      float2 rh[QH];
-      lds_pairs(rh, tp + 3 * QP + s * 3 * QP);
-#pragma unroll
-      for (int h = 0; h < QH; ++h) P[h] = __fmul2_rn(P[h], rh[h]);  // EXTEND
-    }
-  }
-  {
-    float2 hh[QH];
-    lds_pairs(hh, tp + 2 * QP);
-#pragma unroll
-    for (int h = 0; h < QH; ++h) W[h] = __fmul2_rn(P[h], hh[h]);  // W_q = h_q P_q
-  }
-#pragma unroll 1
-  for (int i = 0; i < k; ++i) {
-    const int4 ri = E[i];
-    float2 ai[QH], y[QH];
-    lds_pairs(ai, tp + 3 * QP + i * 3 * QP + 2 * QP);
-    const bool oi = (om >> i) & 1u;
-    float2 ph = make_float2(0.f, 0.f), g = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int h = 0; h < QH; ++h) {
-      const float2 u = oi ? ai[h] : G[h];  // UNWIND(i) folded into u
-      y[h] = __fmul2_rn(W[h], u);
-      ph = __ffma2_rn(y[h], make_float2(2.f, 2.f), ph);  // phi_i = 2 sum_q W_q u_iq
-      g = __ffma2_rn(y[h], G[h], g);
-    }
-    sT[ab[0] + ri.w + ri.z] += ph.x + ph.y;  // Eq. 6 applied at flush
-    const float yg = g.x + g.y;
-#pragma unroll 1
-    for (int j = i + 1; j < k; ++j) {
-      const int cell = ri.w + E[j].z;
-      float2 aj[QH];
-      lds_pairs(aj, tp + 3 * QP + j * 3 * QP + 2 * QP);
-      float2 s2 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int h = 0; h < QH; ++h) s2 = __ffma2_rn(y[h], aj[h], s2);
-      sT[ab[0] + cell] += ((om >> j) & 1u) ? (s2.x + s2.y) : yg;
-    }
-  }
-}
-
 // ------------------------------------------------------------- dispatch
 
 // Small Q: all R rows of the lane at once (shared table loads, R-way ILP).
@@ -981,47 +920,19 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
                 inter_run<T, 4, 1, false>(k, n_run, E, tab, gam, xb1, ab1);
               }
               break;
-            case 5:
-              if constexpr (sizeof(T) == 4 && (GTS_INTER_X2_PATH & (1 << 5))) {
-                for (int p = 0; p < n_run; ++p)
-                  inter_path_x2<5>(k, E + p * k, reinterpret_cast<const float*>(tab) + p * words,
-                                   reinterpret_cast<const float*>(gam), xb1, ab1);
-              } else {
-                inter_run<T, 5, 1, (GTS_INTER_REGACC & (1 << 5)) != 0>(k, n_run, E, tab, gam, xb1, ab1);
-              }
-              break;
+            case 5: inter_run<T, 5, 1, (GTS_INTER_REGACC & (1 << 5)) != 0>(k, n_run, E, tab, gam, xb1, ab1); break;
             case 6:
-              if constexpr (sizeof(T) == 4 && (GTS_INTER_X2_PATH & (1 << 6))) {
-                for (int p = 0; p < n_run; ++p)
-                  inter_path_x2<6>(k, E + p * k, reinterpret_cast<const float*>(tab) + p * words,
-                                   reinterpret_cast<const float*>(gam), xb1, ab1);
-                break;
-              } else if constexpr (sizeof(T) == 4) {
+              if constexpr (sizeof(T) == 4) {
                 inter_run<T, 6, 1, (GTS_INTER_REGACC & (1 << 6)) != 0>(k, n_run, E, tab, gam, xb1, ab1);
                 break;
               }
               [[fallthrough]];
             case 7:
-              if constexpr (sizeof(T) == 4 && (GTS_INTER_X2_PATH & (1 << 7))) {
-                if (q == 7) {
-                  for (int p = 0; p < n_run; ++p)
-                    inter_path_x2<7>(k, E + p * k, reinterpret_cast<const float*>(tab) + p * words,
-                                     reinterpret_cast<const float*>(gam), xb1, ab1);
-                  break;
-                }
-              } else if constexpr (sizeof(T) == 4) {
+              if constexpr (sizeof(T) == 4) {
                 if (q == 7) { inter_run<T, 7, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break; }
               }
               [[fallthrough]];
             default:
-              if constexpr (sizeof(T) == 4 && (GTS_INTER_X2_PATH & (1 << 8))) {
-                if (q == 8) {
-                  for (int p = 0; p < n_run; ++p)
-                    inter_path_x2<8>(k, E + p * k, reinterpret_cast<const float*>(tab) + p * words,
-                                     reinterpret_cast<const float*>(gam), xb1, ab1);
-                  break;
-                }
-              }
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
 #define GTS_IP(QQ) case QQ: inter_path<T, QQ, 1, false>(k, E + p * k, tab + p * words, gam, xb1, ab1); break;
@@ -1073,7 +984,7 @@ __host__ __device__ constexpr int tile_words_per_warp() {
 // slot map (tile_w = max slots + 1, odd: lanes = rows hit distinct banks), so
 // identity maps of M features cost M + 1 words per row, not S + 1.
 #ifndef GTS_XG_FIXED_STRIDE
-#define GTS_XG_FIXED_STRIDE 1  // global-X SHAP kernels: phi tile row stride S + 1 (compile time) or the blob's widest map + 1
+#define GTS_XG_FIXED_STRIDE 0  // global-X SHAP kernels: phi tile row stride S + 1 (compile time) or the blob's widest map + 1
 #endif
 #ifndef GTS_XG_MIN_S
 #define GTS_XG_MIN_S 32  // SHAP kernels with >= this many slots read X from feature-major global memory
@@ -1118,7 +1029,8 @@ __host__ __device__ constexpr int acc_stride(int tile_w) {
 #define GTS_SHAP_W64 4  // no X tile (kXg): 4 warps x 64 rows x 2 blocks fit the phi tiles
 #endif
 #ifndef GTS_SHAP_B64
-#define GTS_SHAP_B64 2
+#define GTS_SHAP_B64 3  // 3 blocks x 4 warps x 64 rows per SM (168 registers, runtime tile stride, 8 KB chunks):
+                        // covtype 1.44e4 -> 1.64e4 rows/s (profiles/r02j)
 #endif
 template <typename T, bool kInter, int S>
 struct Cfg {
