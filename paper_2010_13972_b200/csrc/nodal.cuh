@@ -1187,38 +1187,55 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
     if (dirty) {
       __syncwarp();
       if constexpr (kInter) {
-        const int total = ROWS * cur_slots;  // (row, slot) pairs, slot fastest
-        for (int idx = lane; idx < total; idx += 32) {
-          const int rr = idx / cur_slots, i = idx - rr * cur_slots;
-          const int fi = slotmap[cur_map_begin + i];
-          const int64_t rg = row0 + rr;
-          const T* tile = sT + o_acc + (tile_row0 + rr) * AS;
-          const int rbi = tri_row_base(i, S);
-          if (rg < a.n_rows) {
-            T* base = out + ((size_t)rg * a.G + cur_group) * (size_t)M1 * M1;
-            // the diagonal cell holds sum phi_i; Eq. 6: phi_ii = phi_i - sum_{j != i} phi_ij
-            T rowsum = (T)0;
-            for (int j = 0; j < cur_slots; ++j)
-              if (j != i) rowsum += tile[j < i ? tri_row_base(j, S) + i : rbi + j];
-            const T d = tile[rbi + i] - rowsum;
-            if (d != (T)0) atomicAdd(base + (size_t)fi * M1 + fi, d);
-            // fused call: the diagonal cell before Eq. 6 is the tile's SHAP value phi_i
-            if (a.out_phi != nullptr && tile[rbi + i] != (T)0)
-              atomicAdd(static_cast<T*>(a.out_phi) + ((size_t)rg * a.G + cur_group) * M1 + fi, tile[rbi + i]);
-            for (int j = i + 1; j < cur_slots; ++j) {
-              const T v = tile[rbi + j];
-              if (v != (T)0) {
-                const int fj = slotmap[cur_map_begin + j];
-                atomicAdd(base + (size_t)fi * M1 + fj, v);
-                if (!a.upper_only) atomicAdd(base + (size_t)fj * M1 + fi, v);
+        // lane = row: every lane walks its own row's upper triangle (cell
+        // offsets are compile-time constants, rows have an odd stride, so no
+        // bank conflicts), sums the Eq. 6 row sums in registers, zeroes the
+        // cells it read and issues one RED per non-zero cell.
+        int fm[S];  // slot -> feature (uniform loads)
+#pragma unroll
+        for (int j = 0; j < S; ++j) fm[j] = j < cur_slots ? __ldg(slotmap + cur_map_begin + j) : 0;
+#pragma unroll 1
+        for (int r = 0; r < R; ++r) {
+          const int64_t rg = row0 + r * 32 + lane;
+          const bool ok_r = rg < a.n_rows;
+          T* const tile = sT + ab[r];
+          T* const base = out + ((size_t)(ok_r ? rg : 0) * a.G + cur_group) * (size_t)M1 * M1;
+          T rs[S];
+#pragma unroll
+          for (int i = 0; i < S; ++i) rs[i] = (T)0;
+#pragma unroll
+          for (int i = 0; i < S; ++i) {
+            if (i < cur_slots) {
+#pragma unroll
+              for (int j = i + 1; j < S; ++j) {
+                if (j < cur_slots) {
+                  const int c = i * (2 * S - i - 1) / 2 + j;  // tri_row_base(i, S) + j
+                  const T v = tile[c];
+                  tile[c] = (T)0;
+                  rs[i] += v;
+                  rs[j] += v;
+                  if (ok_r && v != (T)0) {
+                    atomicAdd(base + (size_t)fm[i] * M1 + fm[j], v);
+                    if (!a.upper_only) atomicAdd(base + (size_t)fm[j] * M1 + fm[i], v);
+                  }
+                }
               }
             }
           }
+#pragma unroll
+          for (int i = 0; i < S; ++i) {
+            if (i < cur_slots) {
+              const int c = i * (2 * S - i - 1) / 2 + i;
+              const T di = tile[c];  // sum of phi_i; Eq. 6: phi_ii = phi_i - sum_{j != i} phi_ij
+              tile[c] = (T)0;
+              const T d = di - rs[i];
+              if (ok_r && d != (T)0) atomicAdd(base + (size_t)fm[i] * (M1 + 1), d);
+              // fused call: the diagonal cell before Eq. 6 is the tile's SHAP value phi_i
+              if (ok_r && a.out_phi != nullptr && di != (T)0)
+                atomicAdd(static_cast<T*>(a.out_phi) + ((size_t)rg * a.G + cur_group) * M1 + fm[i], di);
+            }
+          }
         }
-        __syncwarp();
-        // zero the tiles (interaction rows are read across lanes above, so only now)
-        for (int rr = 0; rr < ROWS; ++rr)
-          for (int c = lane; c < AW; c += 32) sT[o_acc + (tile_row0 + rr) * AS + c] = (T)0;
       } else {
         // lane = slot, rows walked in order: consecutive lanes hit consecutive
         // features of one row (coalesced RED); each lane zeroes the cells it read
