@@ -45,6 +45,9 @@
                                  // (measured, profiles/r02h: 5, 6, 7 cost adult 12-16 %; a paired-node
                                  // per-path variant for Q >= 5 cost 28 %, r02j)
 #endif
+#ifndef GTS_INTER_RMW_BLOCK
+#define GTS_INTER_RMW_BLOCK 4  // interaction runs without register cells: tile read-modify-writes per block of cells
+#endif
 #ifndef GTS_INTER_REGACC
 #define GTS_INTER_REGACC 0  // bit Q: interaction runs with Q nodes keep the run's pair cells in registers
 #endif
@@ -161,13 +164,13 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
     const bool valid = (s < KM - 1 || s < k);
-    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
-    slot[s] = e.z;
-    const T* px = xg + (uint32_t)(e.w * cs + xb[0]);  // kXg: the lane's R rows are 32 apart
+    slot[s] = valid ? E[s].z : 0;
+    const int feat = kXg && valid ? E[s].w : 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = (T)0;
-      xv[r][s] = kXg ? __ldg(px + r * 32) : load_x<T, NT, false>(sT, xb[r], e, xg, cs);
+      if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(feat * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
+      else xv[r][s] = sT[xb[r] + (NT == 2 ? slot[s] / (int)sizeof(T) : slot[s])];
     }
   }
   for (int p = 0; p < n_run; ++p) {
@@ -274,13 +277,13 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
     const bool valid = (s < KM - 1 || s < k);
-    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
-    slot[s] = e.z;
-    const float* px = xg + (uint32_t)(e.w * cs + xb[0]);  // kXg: the lane's R rows are 32 apart
+    slot[s] = valid ? E[s].z : 0;
+    const int feat = kXg && valid ? E[s].w : 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = make_float2(0.f, 0.f);
-      xv[r][s] = kXg ? __ldg(px + r * 32) : load_x<float, NT, false>(sT, xb[r], e, xg, cs);
+      if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(feat * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
+      else xv[r][s] = sT[xb[r] + (NT == 2 ? slot[s] / (int)sizeof(float) : slot[s])];
     }
   }
   for (int p = 0; p < n_run; ++p) {
@@ -494,10 +497,6 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int c = 0; c < (kRegAcc ? NC : 1); ++c) acc[r][c] = (T)0;
-  auto add = [&](int r, int c, int i, int j, T v) {
-    if constexpr (kRegAcc) acc[r][c] += v;
-    else sT[ab[r] + rb[i] + slot[j]] += v;
-  };
   for (int p = 0; p < n_run; ++p) {
     const int4* Ep = E + p * k;
     const T* tp = tab + p * words;
@@ -582,6 +581,11 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
           phi[r] = a;
           yg[r] = g;
         }
+        // !kRegAcc: the cells (i, j) of one path are distinct, so they are
+        // updated in blocks of kB: kB values, kB loads, then kB stores (in
+        // program order the compiler must assume a store may alias the next load)
+        constexpr int kB = GTS_INTER_RMW_BLOCK;
+        T pv[R][kRegAcc ? 1 : kB];
 #pragma unroll
         for (int j = i + 1; j < KM; ++j) {
           if (j < KM - 1 || j < k) {
@@ -610,7 +614,29 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
                   for (int q = 0; q < Q; ++q) v = fma(y[r][q], aj[q], v);
                   v = ((om[r] >> j) & 1u) ? v : yg[r];
                 }
-                add(r, c, i, j, v);
+                if constexpr (kB > 1) pv[r][(j - i - 1) % kB] = v;
+                else sT[ab[r] + rb[i] + slot[j]] += v;
+              }
+            }
+          }
+          if constexpr (!kRegAcc && kB > 1) {
+            // flush the block after its last pair (or after the row's last pair)
+            if ((j - i) % kB == 0 || j == KM - 1) {
+              const int j0 = j - ((j - i - 1) % kB);
+              T old[R][kB];
+#pragma unroll
+              for (int b = 0; b < kB; ++b) {
+                const int jj = j0 + b;
+                if (jj <= j && (jj < KM - 1 || jj < k))
+#pragma unroll
+                  for (int r = 0; r < R; ++r) old[r][b] = sT[ab[r] + rb[i] + slot[jj]];
+              }
+#pragma unroll
+              for (int b = 0; b < kB; ++b) {
+                const int jj = j0 + b;
+                if (jj <= j && (jj < KM - 1 || jj < k))
+#pragma unroll
+                  for (int r = 0; r < R; ++r) sT[ab[r] + rb[i] + slot[jj]] = old[r][b] + pv[r][b];
               }
             }
           }
@@ -621,7 +647,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if constexpr (kRegAcc) acc[r][cdiag] = phi[r];
-          else add(r, cdiag, i, i, phi[r]);
+          else sT[ab[r] + rb[i] + slot[i]] += phi[r];
         }
       } else {
         c += KM - i;
@@ -819,7 +845,10 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
 // Small Q: all R rows of the lane at once (shared table loads, R-way ILP).
 // Larger Q: the lane's rows one after the other, which bounds the register
 // footprint of the whole kernel by the small-Q instantiations.
-template <typename T, int R, bool kInter, int NT, bool kXg>
+// QM: the largest Q a kernel with S slots can meet (k <= S, so Q <= S / 2);
+// larger cases are compiled out, which bounds the kernel's register budget by
+// the runs it can actually execute.
+template <typename T, int R, bool kInter, int NT, bool kXg, int QM>
 __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E0, const T* __restrict__ table,
                                              const T* __restrict__ gauss, const int (&xb)[R], const int (&ab)[R],
                                              const T* __restrict__ xg, int cs) {
@@ -831,7 +860,7 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
     // fp32: paired-node FFMA2 runs (Q >= 2); Q = 1 has nothing to pair
     switch (q) {
       case 1: shap_run<T, 1, R, NT, kXg>(k, n_run, E, tab, xb, ab, xg, cs); break;
-#define GTS_RUN(QQ) case QQ: shap_run_x2<QQ, R, NT, kXg>(k, n_run, E, reinterpret_cast<const float*>(tab), xb, ab, \
+#define GTS_RUN(QQ) case QQ: if constexpr (QQ <= QM) shap_run_x2<QQ, R, NT, kXg>(k, n_run, E, reinterpret_cast<const float*>(tab), xb, ab, \
                                                          reinterpret_cast<const float*>(xg), cs); break;
       GTS_RUN(2) GTS_RUN(3) GTS_RUN(4)
 #if GTS_X2_R2_QMAX >= 5
@@ -846,14 +875,14 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
         for (int r = 0; r < R; ++r) {
           const int xb1[1] = {xb[r]}, ab1[1] = {ab[r]};
           switch (q) {
-#define GTS_RUN1(QQ) case QQ: shap_run_x2<QQ, 1, NT, kXg>(k, n_run, E, reinterpret_cast<const float*>(tab), xb1, ab1, \
+#define GTS_RUN1(QQ) case QQ: if constexpr (QQ <= QM) shap_run_x2<QQ, 1, NT, kXg>(k, n_run, E, reinterpret_cast<const float*>(tab), xb1, ab1, \
                                                            reinterpret_cast<const float*>(xg), cs); break;
             GTS_RUN1(5) GTS_RUN1(6) GTS_RUN1(7) GTS_RUN1(8)
 #undef GTS_RUN1
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
-#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1, NT, kXg>(k, E + p * k, tab + p * words, xb1, ab1, xg, cs); break;
+#define GTS_DYN(QQ) case QQ: if constexpr (QQ <= QM) shap_path_dyn<T, QQ, 1, NT, kXg>(k, E + p * k, tab + p * words, xb1, ab1, xg, cs); break;
                   GTS_DYN(9) GTS_DYN(10) GTS_DYN(11) GTS_DYN(12) GTS_DYN(13) GTS_DYN(14) GTS_DYN(15) GTS_DYN(16)
 #undef GTS_DYN
                   default: break;
@@ -864,7 +893,7 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
     }
   } else if constexpr (!kInter) {
     switch (q) {
-#define GTS_RUN(QQ) case QQ: shap_run<T, QQ, R, NT, kXg>(k, n_run, E, tab, xb, ab, xg, cs); break;
+#define GTS_RUN(QQ) case QQ: if constexpr (QQ <= QM) shap_run<T, QQ, R, NT, kXg>(k, n_run, E, tab, xb, ab, xg, cs); break;
       GTS_RUN(1) GTS_RUN(2) GTS_RUN(3) GTS_RUN(4)
 #undef GTS_RUN
       default:
@@ -872,13 +901,13 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
         for (int r = 0; r < R; ++r) {
           const int xb1[1] = {xb[r]}, ab1[1] = {ab[r]};
           switch (q) {
-#define GTS_RUN1(QQ) case QQ: shap_run<T, QQ, 1, NT, kXg>(k, n_run, E, tab, xb1, ab1, xg, cs); break;
+#define GTS_RUN1(QQ) case QQ: if constexpr (QQ <= QM) shap_run<T, QQ, 1, NT, kXg>(k, n_run, E, tab, xb1, ab1, xg, cs); break;
             GTS_RUN1(5) GTS_RUN1(6) GTS_RUN1(7) GTS_RUN1(8)
 #undef GTS_RUN1
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
-#define GTS_DYN(QQ) case QQ: shap_path_dyn<T, QQ, 1, NT, kXg>(k, E + p * k, tab + p * words, xb1, ab1, xg, cs); break;
+#define GTS_DYN(QQ) case QQ: if constexpr (QQ <= QM) shap_path_dyn<T, QQ, 1, NT, kXg>(k, E + p * k, tab + p * words, xb1, ab1, xg, cs); break;
                   GTS_DYN(9) GTS_DYN(10) GTS_DYN(11) GTS_DYN(12) GTS_DYN(13) GTS_DYN(14) GTS_DYN(15) GTS_DYN(16)
 #undef GTS_DYN
                   default: break;
@@ -920,22 +949,24 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
                 inter_run<T, 4, 1, false>(k, n_run, E, tab, gam, xb1, ab1);
               }
               break;
-            case 5: inter_run<T, 5, 1, (GTS_INTER_REGACC & (1 << 5)) != 0>(k, n_run, E, tab, gam, xb1, ab1); break;
+            case 5:
+              if constexpr (QM >= 5) inter_run<T, 5, 1, (GTS_INTER_REGACC & (1 << 5)) != 0>(k, n_run, E, tab, gam, xb1, ab1);
+              break;
             case 6:
-              if constexpr (sizeof(T) == 4) {
+              if constexpr (sizeof(T) == 4 && QM >= 6) {
                 inter_run<T, 6, 1, (GTS_INTER_REGACC & (1 << 6)) != 0>(k, n_run, E, tab, gam, xb1, ab1);
                 break;
               }
               [[fallthrough]];
             case 7:
-              if constexpr (sizeof(T) == 4) {
+              if constexpr (sizeof(T) == 4 && QM >= 7) {
                 if (q == 7) { inter_run<T, 7, 1, false>(k, n_run, E, tab, gam, xb1, ab1); break; }
               }
               [[fallthrough]];
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
-#define GTS_IP(QQ) case QQ: inter_path<T, QQ, 1, false>(k, E + p * k, tab + p * words, gam, xb1, ab1); break;
+#define GTS_IP(QQ) case QQ: if constexpr (QQ <= QM) inter_path<T, QQ, 1, false>(k, E + p * k, tab + p * words, gam, xb1, ab1); break;
                   GTS_IP(6) GTS_IP(7) GTS_IP(8) GTS_IP(9) GTS_IP(10) GTS_IP(11) GTS_IP(12) GTS_IP(13)
                   GTS_IP(14) GTS_IP(15) GTS_IP(16)
 #undef GTS_IP
@@ -1313,7 +1344,8 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
       const T* tab = reinterpret_cast<const T*>(sP + c.n_paths);
       for (int p = 0; p < c.n_paths;) {
         const int4 ph = sP[p];
-        run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S), kXg>(ph, sE, tab, sT, xb, ab, X, (int)a.col_stride);
+        run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S), kXg, (S / 2 < kQMax ? S / 2 : kQMax)>(
+            ph, sE, tab, sT, xb, ab, X, (int)a.col_stride);
         p += ph.x >> 16;
       }
       dirty = true;
