@@ -19,7 +19,9 @@ packed path table is resident (extract -> pack -> blob runs once per model,
 PAPER.md:528; reported as `preprocess_ms` and in the cold `e2e_cold`).  Rows
 are sharded across ranks (weak scaling); rank 0 alone builds the blob and ONE
 NCCL broadcast replicates it.  At N=1 the line also carries `extra` results
-for cal_housing-med and adult-large (mode both).  Rank 0 prints one JSON line.
+for the other BASELINE configs: cal_housing-med and adult-large (mode both),
+covtype-large interactions, fashion_mnist-med SHAP and interactions.  Rank 0
+prints one JSON line.
 """
 from __future__ import annotations
 
@@ -58,8 +60,9 @@ def parse():
                     help="rows per timed step; steps rotate through windows of the dataset (0 = all rows)")
     ap.add_argument("--mode", choices=["both", "shap", "interactions"], default="shap")
     ap.add_argument("--extras", default="auto",
-                    help="comma list workload:mode:rows timed after the main run at N=1 "
-                         "('auto' = cal_housing-med:both:1048576,adult-large:both:65536; 'none')")
+                    help="comma list workload:mode:rows timed after the main run at N=1 ('auto' = "
+                         "cal_housing-med:both:1048576, adult-large:both:65536, covtype-large:interactions:4096, "
+                         "fashion_mnist-med:shap:65536, fashion_mnist-med:interactions:1024; 'none')")
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
     ap.add_argument("--layout", choices=["nodal", "warp_bins"], default="nodal")
     ap.add_argument("--pack", default="bfd")
@@ -607,7 +610,9 @@ def run_ours(args):
 
     extras = None
     if world == 1 and rank == 0 and args.extras != "none":
-        spec = ("cal_housing-med:both:1048576,adult-large:both:65536" if args.extras == "auto" else args.extras)
+        spec = ("cal_housing-med:both:1048576,adult-large:both:65536,covtype-large:interactions:4096,"
+                "fashion_mnist-med:shap:65536,fashion_mnist-med:interactions:1024" if args.extras == "auto"
+                else args.extras)
         extras = {}
         for item in spec.split(","):
             name, xmode, xrows = item.split(":")
