@@ -150,6 +150,12 @@ def test_nodal_blob_invariants(name, slots):
         a, bb = view["path_offset"][q] + 1, view["path_offset"][q + 1]
         if bb > a:
             ref.setdefault(tuple(view["feature"][a:bb]), []).append((float(view["v"][q]), view["zero_fraction"][a:bb]))
+    nt = 2 if hd["S"] > 16 else 3  # SHAP-only blobs drop h and alpha (blob_format.h)
+
+    def slot_of(el):
+        # element record {lo, hi, slot, w}: nt = 3 stores the slot, nt = 2 its byte offset (8-byte T here)
+        return el[:, 2] if nt == 3 else el[:, 2] // 8
+
     seen = 0
     for c in chunks:
         mp = smap[c["slotmap_begin"]:c["slotmap_begin"] + c["n_slots"]]
@@ -163,17 +169,21 @@ def test_nodal_blob_invariants(name, slots):
             run = P[i, 0] >> 16
             assert run >= 1
             k = P[i, 0] & 0xFF
-            feats0 = tuple(mp[E[P[i, 2]:P[i, 2] + k, 2]])
+            feats0 = tuple(mp[slot_of(E[P[i, 2]:P[i, 2] + k])])
             for j in range(run):
                 kk, Q, e0, t0 = P[i + j, 0] & 0xFF, P[i + j, 1], P[i + j, 2], P[i + j, 3]
                 QP = (Q + 3) & ~3
                 assert kk == k and Q == (k + 1) // 2
                 el = E[e0:e0 + k]
-                feats = tuple(mp[el[:, 2]])
+                sl = slot_of(el)
+                feats = tuple(mp[sl])
                 assert feats == feats0
-                np.testing.assert_array_equal(el[:, 3], el[:, 2] * (2 * hd["S"] - el[:, 2] - 1) // 2)
+                if nt == 3:  # slot, upper-triangle row base of the slot
+                    np.testing.assert_array_equal(el[:, 3], sl * (2 * hd["S"] - sl - 1) // 2)
+                else:  # slot byte offset in a tile row, the feature itself (global-X kernels)
+                    np.testing.assert_array_equal(el[:, 2] % 8, 0)
+                    np.testing.assert_array_equal(el[:, 3], np.array(feats))
                 t, wq = g[Q - 1, 0, :Q], g[Q - 1, 1, :Q]
-                nt = 2 if hd["S"] > 16 else 3  # SHAP-only blobs drop h and alpha (blob_format.h)
                 d = tab[t0 + QP:t0 + QP + Q]
                 v = float(-d[0] * (1 - t[0]) / wq[0])
                 cands = ref[feats]
