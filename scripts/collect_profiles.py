@@ -42,7 +42,7 @@ def rep_traffic(rep):
         return {}
     hdr, units = rows[0], rows[1]
     res = collections.defaultdict(list)
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     for r in rows[2:]:
         try:
             b = 0.0
