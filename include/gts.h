@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define GTS_ABI_VERSION 3  /* 3: blob uses (SHAP / interactions) recorded in the info; 32-slot interaction blobs */
+#define GTS_ABI_VERSION 4  /* 4: split bounds in the nodal rho rows; 3: blob uses recorded in the info, 32-slot interaction blobs */
 #define GTS_WARP_CAPACITY 32 /* lanes per warp = bin capacity B */
 
 typedef enum gts_status {

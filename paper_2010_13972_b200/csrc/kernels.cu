@@ -38,6 +38,14 @@ namespace gts {
 gts_status fail(gts_status st, const char* fmt, ...);
 }
 
+// The library is built from several compilations of this file (_build.py,
+// in parallel): GTS_PART = 0 holds everything except the NODAL launches,
+// GTS_PART = 1..4 instantiate launch_nodal (and so the nodal kernels) for
+// {fp32, fp64} x {SHAP, interactions}.
+#ifndef GTS_PART
+#define GTS_PART 0
+#endif
+
 namespace gts {
 namespace {
 
@@ -197,9 +205,11 @@ size_t nodal_smem_bytes(const gts_blob_info* info) {
   return (size_t)nodal::staging_byte_offset<T, S, W, R, kInter>(shap_tile_w(info)) + 2 * nodal_buffer_bytes(info) + 16;
 }
 
+}  // namespace
+namespace nl {
 template <typename T, bool kInter, int S>
 gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const void* d_X, int64_t n_rows, int64_t rs,
-                        int64_t cs, void* out, cudaStream_t st, void* out_phi = nullptr) {
+                        int64_t cs, void* out, cudaStream_t st, void* out_phi) {
   constexpr int W = nodal::Cfg<T, kInter, S>::W;
   constexpr int R = nodal::Cfg<T, kInter, S>::R;
   auto kern = nodal::nodal_kernel<T, S, W, R, kInter>;
@@ -321,6 +331,33 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   return cuda_check("mirror kernel launch");
 }
 
+#define GTS_LN_SIG(T, I, S)                                                                                       \
+  gts_status launch_nodal<T, I, S>(const gts_blob_info*, const char*, const void*, int64_t, int64_t, int64_t, void*, \
+                                   cudaStream_t, void*)
+#if GTS_PART == 0
+#define GTS_LN(T, I, S) extern template GTS_LN_SIG(T, I, S);
+#else
+#define GTS_LN(T, I, S) template GTS_LN_SIG(T, I, S);
+#endif
+#if GTS_PART == 0 || GTS_PART == 1
+GTS_LN(float, false, 8) GTS_LN(float, false, 16) GTS_LN(float, false, 32) GTS_LN(float, false, 64)
+#endif
+#if GTS_PART == 0 || GTS_PART == 2
+GTS_LN(float, true, 8) GTS_LN(float, true, 16) GTS_LN(float, true, 32)
+#endif
+#if GTS_PART == 0 || GTS_PART == 3
+GTS_LN(double, false, 8) GTS_LN(double, false, 16) GTS_LN(double, false, 32) GTS_LN(double, false, 64)
+#endif
+#if GTS_PART == 0 || GTS_PART == 4
+GTS_LN(double, true, 8) GTS_LN(double, true, 16) GTS_LN(double, true, 32)
+#endif
+#undef GTS_LN
+#undef GTS_LN_SIG
+}  // namespace nl
+#if GTS_PART == 0
+namespace {
+using nl::launch_nodal;
+
 template <typename T, bool kInter>
 gts_status launch_nodal_s(const gts_blob_info* info, const char* d_blob, const void* d_X, int64_t n_rows,
                           int64_t rs, int64_t cs, void* out, cudaStream_t st, void* out_phi = nullptr) {
@@ -330,7 +367,7 @@ gts_status launch_nodal_s(const gts_blob_info* info, const char* d_blob, const v
     case 32: return launch_nodal<T, kInter, 32>(info, d_blob, d_X, n_rows, rs, cs, out, st, out_phi);
     case 64:
       if constexpr (kInter) break;
-      else return launch_nodal<T, kInter, 64>(info, d_blob, d_X, n_rows, rs, cs, out, st);
+      else return launch_nodal<T, kInter, 64>(info, d_blob, d_X, n_rows, rs, cs, out, st, nullptr);
     default: break;
   }
   return fail(GTS_ERR_INVALID_ARGUMENT, "unsupported max_slots %d", info->max_slots);
@@ -468,8 +505,10 @@ gts_status run_fused(const gts_blob_info* info, const void* d_blob, const void* 
 }
 
 }  // namespace
+#endif  // GTS_PART == 0
 }  // namespace gts
 
+#if GTS_PART == 0
 extern "C" {
 
 gts_status gts_shap(const gts_blob_info* info, const void* d_blob, const void* d_X, int64_t n_rows, int64_t ld_x,
@@ -551,4 +590,4 @@ int32_t gts_launches_per_call(const gts_blob_info* info, int32_t interactions) {
 }
 
 }  // extern "C"
-
+#endif  // GTS_PART == 0

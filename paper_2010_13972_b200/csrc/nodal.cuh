@@ -58,9 +58,6 @@
 #ifndef GTS_SHAP_R_WIDE
 #define GTS_SHAP_R_WIDE 1  // rows per lane of the fp32 SHAP kernel with 32 or 64 slots
 #endif
-#ifndef GTS_SHAP_RECOMPUTE_O
-#define GTS_SHAP_RECOMPUTE_O 0  // scalar SHAP runs: recompute o_s for UNWIND instead of keeping o-bits
-#endif
 #ifndef GTS_SHAP_R8
 #define GTS_SHAP_R8 4  // rows per lane of the fp32 SHAP kernel with 8 slots (measured: 4 > 2)
 #endif
@@ -115,6 +112,71 @@ __device__ __forceinline__ void lds_pairs(float2 (&dst)[N], const float* src) {
   }
 }
 
+// Offsets (T words) inside a path's nodal table (blob_format.h): element s's
+// rho row (with the split bounds at BO), its C' row (SHAP) and alpha row
+// (interactions; NT = 3).
+template <int Q, int NT>
+struct Lay {
+  static constexpr int QP = (Q + 3) & ~3, BO = (Q + 1) & ~1, RW = (BO + 2 + 3) & ~3, ES = RW + (NT - 1) * QP;
+  static_assert(BO == nodal_bo(Q) && RW == nodal_rw(Q) && ES == nodal_es(Q, NT), "table layout");
+  __device__ static __forceinline__ int rho(int s) { return NT * QP + s * ES; }
+  __device__ static __forceinline__ int cp(int s) { return NT * QP + s * ES + RW; }
+  __device__ static __forceinline__ int al(int s) { return NT * QP + s * ES + RW + QP; }
+};
+
+// The first NW words of a 16-byte aligned row by 16-byte loads (an 8-byte
+// load for a trailing pair of fp32 words).
+template <typename T, int NW>
+__device__ __forceinline__ void lds_words(T (&w)[NW], const T* src) {
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int i = 0; i < NW; i += 4) {
+      if (i + 4 <= NW) {
+        const float4 v = *reinterpret_cast<const float4*>(src + i);
+        w[i] = v.x, w[i + 1] = v.y, w[i + 2] = v.z, w[i + 3] = v.w;
+      } else {
+        const float2 v = *reinterpret_cast<const float2*>(src + i);
+        w[i] = v.x, w[i + 1] = v.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NW; i += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(src + i);
+      w[i] = v.x, w[i + 1] = v.y;
+    }
+  }
+}
+
+// rho_s at the Q nodes and the split bounds of element s, from its rho row.
+template <typename T, int Q>
+__device__ __forceinline__ void lds_rho(T (&rho)[Q], T& lo, T& hi, const T* row) {
+  constexpr int BO = (Q + 1) & ~1;
+  T w[BO + 2];
+  lds_words(w, row);
+#pragma unroll
+  for (int q = 0; q < Q; ++q) rho[q] = w[q];
+  lo = w[BO];
+  hi = w[BO + 1];
+}
+
+// fp32: rho_s on packed node pairs (odd Q: the zero pad completes the last pair) and the bounds.
+template <int Q>
+__device__ __forceinline__ void lds_rho_pairs(float2 (&rh)[(Q + 1) / 2], float& lo, float& hi, const float* row) {
+  constexpr int BO = (Q + 1) & ~1;
+  float w[BO + 2];
+  lds_words(w, row);
+#pragma unroll
+  for (int h = 0; h < (Q + 1) / 2; ++h) rh[h] = make_float2(w[2 * h], w[2 * h + 1]);
+  lo = w[BO];
+  hi = w[BO + 1];
+}
+
+template <typename T>
+__device__ __forceinline__ bool in_bounds(T x, T lo, T hi) {
+  return (x >= lo) & (x < hi);  // o = [lower <= x < upper]  (reading G1)
+}
+
 template <typename T>
 __device__ __forceinline__ bool one_fraction(T x, int4 rec) {
   // o = [lower <= x < upper]  (half-open bounds, reading G1)
@@ -157,24 +219,22 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
   constexpr int kRmw = GTS_RMW_REGS / R > 1 ? GTS_RMW_REGS / R : 1;
   T* const sT = reinterpret_cast<T*>(g_smem);
   const int words = nodal_path_words(k, Q, NT);
-  int slot[KM];
-  T acc[R][KM], xv[R][KM], ph0[R];  // the run's slots and this lane's x values, loaded once per run
+  T acc[R][KM], xv[R][KM], ph0[R];  // this lane's x values, loaded once per run
 #pragma unroll
   for (int r = 0; r < R; ++r) ph0[r] = (T)0;
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
     const bool valid = (s < KM - 1 || s < k);
-    slot[s] = valid ? E[s].z : 0;
-    const int feat = kXg && valid ? E[s].w : 0;
+    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = (T)0;
-      if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(feat * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
-      else xv[r][s] = sT[xb[r] + (NT == 2 ? slot[s] / (int)sizeof(T) : slot[s])];
+      if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(e.w * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
+      else xv[r][s] = sT[xb[r] + (NT == 2 ? e.z / (int)sizeof(T) : e.z)];
     }
   }
+  using L = Lay<Q, NT>;
   for (int p = 0; p < n_run; ++p) {
-    const int4* Ep = E + p * k;
     const T* tp = tab + p * words;
     T P[R][Q];
     {
@@ -191,12 +251,11 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        const int4 rec = Ep[s];
-        T rho[Q];
-        lds_vec(rho, tp + NT * QP + s * NT * QP);
+        T rho[Q], lo, hi;
+        lds_rho(rho, lo, hi, tp + L::rho(s));
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const bool o = one_fraction(xv[r][s], rec);
+          const bool o = in_bounds(xv[r][s], lo, hi);
           om[r] |= (uint32_t)o << s;
           if (!o) {
 #pragma unroll
@@ -217,13 +276,10 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
         T C[Q];
-        lds_vec(C, tp + NT * QP + s * NT * QP + QP);
+        lds_vec(C, tp + L::cp(s));
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          bool o;
-          if constexpr (GTS_SHAP_RECOMPUTE_O) o = one_fraction(xv[r][s], Ep[s]);
-          else o = (om[r] >> s) & 1u;
-          if (o) {
+          if ((om[r] >> s) & 1u) {
 #pragma unroll
             for (int q = 0; q < Q; ++q) acc[r][s] = fma(P[r][q], C[q], acc[r][s]);  // UNWIND(s) folded into C'
           }
@@ -234,23 +290,28 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
   // The run's slots are distinct features (merged paths), so the tile cells are
   // updated in groups of kRmw: kRmw loads, then kRmw stores, instead of each
   // read-modify-write waiting for the previous store (the compiler cannot
-  // prove runtime slots distinct, so it keeps them in program order).
+  // prove runtime slots distinct, so it keeps them in program order).  The
+  // slots are re-read from the run head's records here rather than held in
+  // registers through the run.
 #pragma unroll
   for (int s0 = 0; s0 < KM; s0 += kRmw) {
     T old[R][kRmw];
+    int slot[kRmw];
 #pragma unroll
     for (int b = 0; b < kRmw; ++b) {
       const int s = s0 + b;
-      if (s < KM && (s < KM - 1 || s < k))
+      if (s < KM && (s < KM - 1 || s < k)) {
+        slot[b] = E[s].z;
 #pragma unroll
-        for (int r = 0; r < R; ++r) old[r][b] = tile_at<T, NT>(ab[r], slot[s]);
+        for (int r = 0; r < R; ++r) old[r][b] = tile_at<T, NT>(ab[r], slot[b]);
+      }
     }
 #pragma unroll
     for (int b = 0; b < kRmw; ++b) {
       const int s = s0 + b;
       if (s < KM && (s < KM - 1 || s < k))
 #pragma unroll
-        for (int r = 0; r < R; ++r) tile_at<T, NT>(ab[r], slot[s]) = old[r][b] + (acc[r][s] + ph0[r]);
+        for (int r = 0; r < R; ++r) tile_at<T, NT>(ab[r], slot[b]) = old[r][b] + (acc[r][s] + ph0[r]);
     }
   }
 }
@@ -269,7 +330,6 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
   constexpr int kRmw = GTS_RMW_REGS / R > 1 ? GTS_RMW_REGS / R : 1;
   float* const sT = reinterpret_cast<float*>(g_smem);
   const int words = nodal_path_words(k, Q, NT);
-  int slot[KM];
   float xv[R][KM];
   float2 acc[R][KM], ph0[R];
 #pragma unroll
@@ -277,17 +337,16 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
     const bool valid = (s < KM - 1 || s < k);
-    slot[s] = valid ? E[s].z : 0;
-    const int feat = kXg && valid ? E[s].w : 0;
+    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = make_float2(0.f, 0.f);
-      if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(feat * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
-      else xv[r][s] = sT[xb[r] + (NT == 2 ? slot[s] / (int)sizeof(float) : slot[s])];
+      if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(e.w * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
+      else xv[r][s] = sT[xb[r] + (NT == 2 ? e.z / (int)sizeof(float) : e.z)];
     }
   }
+  using L = Lay<Q, NT>;
   for (int p = 0; p < n_run; ++p) {
-    const int4* Ep = E + p * k;
     const float* tp = tab + p * words;
     float2 P[R][QH];
     {
@@ -304,12 +363,12 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        const int4 rec = Ep[s];
         float2 rh[QH];
-        lds_pairs(rh, tp + NT * QP + s * NT * QP);
+        float lo, hi;
+        lds_rho_pairs<Q>(rh, lo, hi, tp + L::rho(s));
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const bool o = one_fraction(xv[r][s], rec);
+          const bool o = in_bounds(xv[r][s], lo, hi);
           om[r] |= (uint32_t)o << s;
           if (!o) {
 #pragma unroll
@@ -330,7 +389,7 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
         float2 Ch[QH];
-        lds_pairs(Ch, tp + NT * QP + s * NT * QP + QP);
+        lds_pairs(Ch, tp + L::cp(s));
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if ((om[r] >> s) & 1u) {
@@ -344,12 +403,15 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 #pragma unroll
   for (int s0 = 0; s0 < KM; s0 += kRmw) {  // grouped read-modify-writes, see shap_run
     float old[R][kRmw];
+    int slot[kRmw];
 #pragma unroll
     for (int b = 0; b < kRmw; ++b) {
       const int s = s0 + b;
-      if (s < KM && (s < KM - 1 || s < k))
+      if (s < KM && (s < KM - 1 || s < k)) {
+        slot[b] = E[s].z;
 #pragma unroll
-        for (int r = 0; r < R; ++r) old[r][b] = tile_at<float, NT>(ab[r], slot[s]);
+        for (int r = 0; r < R; ++r) old[r][b] = tile_at<float, NT>(ab[r], slot[b]);
+      }
     }
 #pragma unroll
     for (int b = 0; b < kRmw; ++b) {
@@ -357,7 +419,7 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
       if (s < KM && (s < KM - 1 || s < k))
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          tile_at<float, NT>(ab[r], slot[s]) = old[r][b] + ((acc[r][s].x + acc[r][s].y) + (ph0[r].x + ph0[r].y));
+          tile_at<float, NT>(ab[r], slot[b]) = old[r][b] + ((acc[r][s].x + acc[r][s].y) + (ph0[r].x + ph0[r].y));
     }
   }
 }
@@ -385,7 +447,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
   for (int s = 0; s < k; ++s) {
     const int4 rec = E[s];
     T rho[Q];
-    lds_vec(rho, tab + NT * QP + s * NT * QP);
+    lds_vec(rho, tab + Lay<Q, NT>::rho(s));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool o = one_fraction(load_x<T, NT, kXg>(sT, xb[r], rec, xg, cs), rec);
@@ -412,7 +474,7 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
   for (int s = 0; s < k; ++s) {
     const int sl = E[s].z;
     T C[Q];
-    lds_vec(C, tab + NT * QP + s * NT * QP + QP);
+    lds_vec(C, tab + Lay<Q, NT>::cp(s));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       T a = ph0[r];
@@ -446,7 +508,7 @@ __device__ __forceinline__ void inter_extend(int k, const int4* __restrict__ E, 
   auto body = [&](int s) {
     const int4 rec = E[s];
     T rho[Q];
-    lds_vec(rho, tp + 3 * QP + s * 3 * QP);
+    lds_vec(rho, tp + Lay<Q, 3>::rho(s));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool o = one_fraction(sT[xb[r] + rec.z], rec);
@@ -497,8 +559,8 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int c = 0; c < (kRegAcc ? NC : 1); ++c) acc[r][c] = (T)0;
+  using L = Lay<Q, 3>;
   for (int p = 0; p < n_run; ++p) {
-    const int4* Ep = E + p * k;
     const T* tp = tab + p * words;
     T P[R][Q];
     uint32_t om[R];
@@ -515,12 +577,11 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        const int4 rec = Ep[s];
-        T rho[Q];
-        lds_vec(rho, tp + 3 * QP + s * 3 * QP);
+        T rho[Q], lo, hi;
+        lds_rho(rho, lo, hi, tp + L::rho(s));
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const bool o = one_fraction(xv[r][s], rec);
+          const bool o = in_bounds(xv[r][s], lo, hi);
           if (o) om[r] |= 1u << s;
           if (!o) {
 #pragma unroll
@@ -547,7 +608,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
       for (int s = 0; s < KM; ++s) {
         if (s < KM - 1 || s < k) {
           T al[Q];
-          lds_vec(al, tp + 3 * QP + s * 3 * QP + 2 * QP);
+          lds_vec(al, tp + L::al(s));
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const bool o = (om[r] >> s) & 1u;
@@ -563,7 +624,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
       if (i < KM - 1 || i < k) {
         T y[R][Q], phi[R], yg[R];
         T ai[Q];
-        if constexpr (!kCacheU) lds_vec(ai, tp + 3 * QP + i * 3 * QP + 2 * QP);
+        if constexpr (!kCacheU) lds_vec(ai, tp + L::al(i));
         const int cdiag = c++;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -590,7 +651,7 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
         for (int j = i + 1; j < KM; ++j) {
           if (j < KM - 1 || j < k) {
             T aj[Q];
-            if constexpr (!kCacheU) lds_vec(aj, tp + 3 * QP + j * 3 * QP + 2 * QP);
+            if constexpr (!kCacheU) lds_vec(aj, tp + L::al(j));
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               if constexpr (kRegAcc) {
@@ -687,21 +748,17 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
 #pragma unroll
   for (int h = 0; h < NP; ++h) G[h] = make_float2(gam[2 * h], gam[2 * h + 1]);
   const float Gt = kTail ? gam[TQ] : 0.f;
-  int slot[KM], rb[KM];
   float xv[KM];
 #pragma unroll
   for (int s = 0; s < KM; ++s) {
     const bool valid = (s < KM - 1 || s < k);
-    const int4 e = valid ? E[s] : make_int4(0, 0, 0, 0);
-    slot[s] = e.z;
-    rb[s] = e.w;
-    xv[s] = sT[xb[0] + e.z];
+    xv[s] = sT[xb[0] + (valid ? E[s].z : 0)];
   }
   float2 acc[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c] = make_float2(0.f, 0.f);
+  using L = Lay<Q, 3>;
   for (int p = 0; p < n_run; ++p) {
-    const int4* Ep = E + p * k;
     const float* tf = tab + p * words;
     const float2* tp = reinterpret_cast<const float2*>(tf);
     float2 P[NP > 0 ? NP : 1];
@@ -712,13 +769,14 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        const bool o = one_fraction(xv[s], Ep[s]);
+        float w[L::BO + 2];
+        lds_words(w, tf + L::rho(s));
+        const bool o = in_bounds(xv[s], w[L::BO], w[L::BO + 1]);
         om |= (uint32_t)o << s;
         if (!o) {
-          const float* rho = tf + 3 * QP + s * 3 * QP;
 #pragma unroll
-          for (int h = 0; h < NP; ++h) P[h] = __fmul2_rn(P[h], reinterpret_cast<const float2*>(rho)[h]);  // EXTEND
-          if constexpr (kTail) Pt *= rho[TQ];
+          for (int h = 0; h < NP; ++h) P[h] = __fmul2_rn(P[h], make_float2(w[2 * h], w[2 * h + 1]));  // EXTEND
+          if constexpr (kTail) Pt *= w[TQ];
         }
       }
     }
@@ -731,7 +789,7 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        const float* al = tf + 3 * QP + s * 3 * QP + 2 * QP;
+        const float* al = tf + L::al(s);
         const bool o = (om >> s) & 1u;
 #pragma unroll
         for (int h = 0; h < NP; ++h) {
@@ -773,6 +831,15 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
       }
     }
   }
+  // the slots (and tri-row bases) are read back from the run head's records
+  // only now, when the path registers are dead
+  int slot[KM], rb[KM];
+#pragma unroll
+  for (int s = 0; s < KM; ++s) {
+    const int4 e = (s < KM - 1 || s < k) ? E[s] : make_int4(0, 0, 0, 0);
+    slot[s] = e.z;
+    rb[s] = e.w;
+  }
   int c = 0;
 #pragma unroll
   for (int i = 0; i < KM; ++i) {
@@ -808,7 +875,7 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
   for (int i = 0; i < k; ++i) {
     const int4 ri = E[i];
     T ai[Q];
-    lds_vec(ai, tp + 3 * QP + i * 3 * QP + 2 * QP);
+    lds_vec(ai, tp + Lay<Q, 3>::al(i));
     T y[R][Q], yg[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -828,7 +895,7 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
     for (int j = i + 1; j < k; ++j) {
       const int cell = ri.w + E[j].z;
       T aj[Q];
-      lds_vec(aj, tp + 3 * QP + j * 3 * QP + 2 * QP);
+      lds_vec(aj, tp + Lay<Q, 3>::al(j));
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         T s1 = (T)0;
@@ -1041,6 +1108,9 @@ __host__ __device__ constexpr int acc_stride(int tile_w) {
 // per-chunk maps of 32) trade warps for rows per lane: the per-path tables
 // are read from shared memory once per lane and used for R rows, which is
 // what bounds these kernels (LSU pipe, profiles/r01g).
+#ifndef GTS_INTER8_W
+#define GTS_INTER8_W 8  // warps per block of the 8-slot fp32 interaction kernel
+#endif
 #ifndef GTS_INTER8_MINB
 #define GTS_INTER8_MINB 2  // resident blocks per SM the 8-slot fp32 interaction kernel's registers are sized for
 #endif
@@ -1073,6 +1143,7 @@ struct Cfg {
                                                        : 1;
   static constexpr int tile_bytes = (int)sizeof(T) * tile_words_per_warp<T, S, R, kInter>();
   static constexpr int W = (sizeof(T) == 4 && kWide) ? (S == 32 ? GTS_SHAP_W32 : GTS_SHAP_W64)
+                           : (sizeof(T) == 4 && kInter && S == 8) ? GTS_INTER8_W
                            : tile_bytes * 8 <= 74 * 1024  ? 8
                            : tile_bytes * 4 <= 80 * 1024  ? 4
                            : tile_bytes * 2 <= 160 * 1024 ? 2

@@ -44,7 +44,7 @@ def test_exports_every_declared_symbol():
 
 def test_version_and_status_strings():
     lib = gts.load()
-    assert lib.gts_abi_version() == 3
+    assert lib.gts_abi_version() == 4
     for code, name in gts.STATUS_NAMES.items():
         assert lib.gts_status_string(code).decode() == name
 
@@ -107,7 +107,7 @@ def test_blob_plan_and_call_argument_errors():
     assert _status(gts.gts_blob_plan, b, 0, 9, 0) == 1
     assert _status(gts.gts_blob_plan, b, 0, 0, 12) == 1
     info = gts.gts_blob_plan(b, gts.GTS_F32, "nodal")
-    assert info.magic == 0x47545342 and info.abi_version == 3 and info.bytes % 256 == 0
+    assert info.magic == 0x47545342 and info.abi_version == 4 and info.bytes % 256 == 0
     with pytest.raises(ValueError):
         gts.gts_blob_write(b, info, np.empty(16, np.uint8))
     # n_rows == 0 is a no-op; argument errors are caught before any CUDA call

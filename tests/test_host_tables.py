@@ -195,15 +195,24 @@ def test_nodal_blob_invariants(name, slots):
                 np.testing.assert_allclose(tab[t0 + QP:t0 + QP + Q], -v * wq / (1 - t), rtol=1e-12, atol=1e-300)
                 if nt == 3:
                     np.testing.assert_allclose(tab[t0 + 2 * QP:t0 + 2 * QP + Q], 0.5 * v * wq, rtol=1e-12, atol=1e-300)
-                rows = tab[t0 + nt * QP:t0 + nt * QP * (k + 1)].reshape(k, nt, QP)[:, :, :Q]
-                np.testing.assert_allclose(rows[:, 0], B / A, rtol=1e-12)
+                # element rows (blob_format.h): rho[RW] with the bounds at BO, C'[QP] (, alpha[QP])
+                BO = (Q + 1) & ~1
+                RW = (BO + 2 + 3) & ~3
+                ES = RW + (nt - 1) * QP
+                rows = tab[t0 + nt * QP:t0 + nt * QP + k * ES].reshape(k, ES)
+                np.testing.assert_allclose(rows[:, :Q], B / A, rtol=1e-12)
+                assert np.all(rows[:, Q:BO] == 0)  # the zero pad of an odd Q's last node pair
                 # C' = C - d: the SHAP constant with the o = 0 share folded out (nodal.cuh shap_run)
-                np.testing.assert_allclose(rows[:, 1], v * wq[None] * ((1 - z[:, None]) / A + 1 / (1 - t[None])),
+                np.testing.assert_allclose(rows[:, RW:RW + Q], v * wq[None] * ((1 - z[:, None]) / A + 1 / (1 - t[None])),
                                            rtol=1e-12, atol=1e-300)
                 if nt == 3:
-                    np.testing.assert_allclose(rows[:, 2], (1 - z[:, None]) / A, rtol=1e-12, atol=1e-300)
+                    np.testing.assert_allclose(rows[:, RW + QP:RW + QP + Q], (1 - z[:, None]) / A, rtol=1e-12, atol=1e-300)
                 lo = E[e0:e0 + k, 0].view(np.float32)
+                hi = E[e0:e0 + k, 1].view(np.float32)
                 assert np.all(lo == lo)  # bounds stored as fp32 bit patterns
+                # the rho row carries the same bounds (as T) for EXTEND's o_s
+                np.testing.assert_array_equal(rows[:, BO], lo.astype(np.float64))
+                np.testing.assert_array_equal(rows[:, BO + 1], hi.astype(np.float64))
                 seen += 1
             i += run
     assert seen == hd["n_kept_paths"] and not any(ref.values())
