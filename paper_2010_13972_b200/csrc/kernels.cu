@@ -212,7 +212,12 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
                         int64_t cs, void* out, cudaStream_t st, void* out_phi) {
   constexpr int W = nodal::Cfg<T, kInter, S>::W;
   constexpr int R = nodal::Cfg<T, kInter, S>::R;
-  auto kern = nodal::nodal_kernel<T, S, W, R, kInter>;
+  constexpr int XG = nodal::xg_enabled<kInter, S>() ? 1 : 0;
+  auto kern = nodal::nodal_kernel<T, S, W, R, kInter, XG>;
+  if constexpr (XG == 1 && GTS_TMEM_X && sizeof(T) == 4 && S == 64 && W == 4 && R * 64 <= 128) {
+    // identity slot map (features = slots < 64): x from TMEM (nodal::load_x)
+    if (info->n_features <= 64) kern = nodal::nodal_kernel<T, S, W, R, kInter, 2>;
+  }
   const size_t smem = nodal_smem_bytes<T, kInter, S>(info);
   if (smem > 227 * 1024) return fail(GTS_ERR_INVALID_ARGUMENT, "chunk staging needs %zu bytes of shared memory", smem);
   void* xt = nullptr;  // padded feature-major scratch copy of X (xg kernels)

@@ -190,10 +190,40 @@ __device__ __forceinline__ bool one_fraction(T x, int4 rec) {
 // coalesced, L1-resident line per warp instruction; the launcher keeps
 // feature * cs + row within 32 bits).  SHAP-only records (NT = 2) hold the
 // slot as a byte offset into a tile row.
-template <typename T, int NT, bool kXg>
+// kXg = 2 (fp32 SHAP with identity maps of <= 64 features): the block's X
+// rows live in tensor memory (TMEM, 12-cycle loads instead of L2 misses: the
+// L1 left beside three blocks' shared memory cannot hold their X rows); each
+// thread owns one TMEM lane, its row r's features at columns r * 64 + f, so
+// cs = the warp's TMEM address (lane quarter) and xb = r * 64.
+//
+// tcgen05.ld / st (.sync.aligned: warp-uniform control flow only, which the
+// row-lane runs are) complete asynchronously: tm_wait_ld, then tm_pin on each
+// loaded value, so that no use of it is scheduled above the wait.
+__device__ __forceinline__ float tm_ld(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+  return __uint_as_float(v);
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_pin(float& v) { asm volatile("" : "+f"(v)); }
+__device__ __forceinline__ void tm_pin(double& v) { asm volatile("" : "+d"(v)); }
+__device__ __forceinline__ void tm_st(uint32_t taddr, float v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v)) : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <typename T, int NT, int kXg>
 __device__ __forceinline__ T load_x(const T* sT, int xb, int4 rec, const T* __restrict__ xg, int cs) {
-  if constexpr (kXg) return __ldg(xg + (uint32_t)(rec.w * cs + xb));
-  else return sT[xb + (NT == 2 ? rec.z / (int)sizeof(T) : rec.z)];
+  if constexpr (kXg == 2) {
+    T v = (T)tm_ld((uint32_t)cs + (uint32_t)(xb + rec.w));
+    tm_wait_ld();
+    tm_pin(v);
+    return v;
+  } else if constexpr (kXg) {
+    return __ldg(xg + (uint32_t)(rec.w * cs + xb));
+  } else {
+    return sT[xb + (NT == 2 ? rec.z / (int)sizeof(T) : rec.z)];
+  }
 }
 
 // The phi tile cell of lane-row ab (word index of its tile row) at a slot
@@ -212,7 +242,7 @@ __device__ __forceinline__ T& tile_at(int ab, int slot) {
 // i.e. an o_s = 1 element costs one predicated FMA chain straight into its
 // accumulator and an o_s = 0 element costs nothing; ph0 is summed once per
 // path into one register per row and added to every slot of the run at its end.
-template <typename T, int Q, int R, int NT, bool kXg>
+template <typename T, int Q, int R, int NT, int kXg>
 __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restrict__ E, const T* __restrict__ tab,
                                          const int (&xb)[R], const int (&ab)[R], const T* __restrict__ xg, int cs) {
   constexpr int QP = QP_<Q>::v, KM = 2 * Q;
@@ -229,9 +259,17 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = (T)0;
-      if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(e.w * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
+      if constexpr (kXg == 2) xv[r][s] = (T)tm_ld((uint32_t)cs + (uint32_t)(xb[r] + e.w));
+      else if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(e.w * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
       else xv[r][s] = sT[xb[r] + (NT == 2 ? e.z / (int)sizeof(T) : e.z)];
     }
+  }
+  if constexpr (kXg == 2) {
+    tm_wait_ld();
+#pragma unroll
+    for (int s = 0; s < KM; ++s)
+#pragma unroll
+      for (int r = 0; r < R; ++r) tm_pin(xv[r][s]);
   }
   using L = Lay<Q, NT>;
   for (int p = 0; p < n_run; ++p) {
@@ -322,7 +360,7 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 // work), predicated per row as before.  Pads (q >= Q) are zero in the table,
 // so P_pad = 0 and they contribute nothing.  acc keeps even/odd node partial
 // sums, folded once per run.
-template <int Q, int R, int NT, bool kXg>
+template <int Q, int R, int NT, int kXg>
 __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __restrict__ E,
                                             const float* __restrict__ tab, const int (&xb)[R], const int (&ab)[R],
                                             const float* __restrict__ xg, int cs) {
@@ -341,9 +379,17 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = make_float2(0.f, 0.f);
-      if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(e.w * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
+      if constexpr (kXg == 2) xv[r][s] = tm_ld((uint32_t)cs + (uint32_t)(xb[r] + e.w));
+      else if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(e.w * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
       else xv[r][s] = sT[xb[r] + (NT == 2 ? e.z / (int)sizeof(float) : e.z)];
     }
+  }
+  if constexpr (kXg == 2) {
+    tm_wait_ld();
+#pragma unroll
+    for (int s = 0; s < KM; ++s)
+#pragma unroll
+      for (int r = 0; r < R; ++r) tm_pin(xv[r][s]);
   }
   using L = Lay<Q, NT>;
   for (int p = 0; p < n_run; ++p) {
@@ -425,7 +471,7 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 }
 
 // One path, element loop not unrolled (large Q); accumulates per element.
-template <typename T, int Q, int R, int NT, bool kXg>
+template <typename T, int Q, int R, int NT, int kXg>
 __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E, const T* __restrict__ tab,
                                               const int (&xb)[R], const int (&ab)[R], const T* __restrict__ xg,
                                               int cs) {
@@ -915,7 +961,7 @@ __device__ __forceinline__ void inter_path(int k, const int4* __restrict__ E, co
 // QM: the largest Q a kernel with S slots can meet (k <= S, so Q <= S / 2);
 // larger cases are compiled out, which bounds the kernel's register budget by
 // the runs it can actually execute.
-template <typename T, int R, bool kInter, int NT, bool kXg, int QM>
+template <typename T, int R, bool kInter, int NT, int kXg, int QM>
 __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E0, const T* __restrict__ table,
                                              const T* __restrict__ gauss, const int (&xb)[R], const int (&ab)[R],
                                              const T* __restrict__ xg, int cs) {
@@ -1084,6 +1130,9 @@ __host__ __device__ constexpr int tile_words_per_warp() {
 #ifndef GTS_XG_FIXED_STRIDE
 #define GTS_XG_FIXED_STRIDE 0  // global-X SHAP kernels: phi tile row stride S + 1 (compile time) or the blob's widest map + 1
 #endif
+#ifndef GTS_TMEM_X
+#define GTS_TMEM_X 1  // fp32 SHAP kernels with identity maps of <= 64 features keep X in TMEM (XG = 2)
+#endif
 #ifndef GTS_XG_MIN_S
 #define GTS_XG_MIN_S 32  // SHAP kernels with >= this many slots read X from feature-major global memory
                          // (measured, profiles/r02f-g: with 2 rows per lane fashion 5.06e5 -> 6.14e5 rows/s,
@@ -1174,11 +1223,26 @@ __device__ __forceinline__ void mbar_fence_init() {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+#ifndef GTS_TMA_POLICY
+#define GTS_TMA_POLICY 0  // L2 policy of the chunk copies: 0 default, 1 evict_normal, 2 evict_last, 3 evict_first
+#endif
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+  if constexpr (GTS_TMA_POLICY == 0) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+  } else {
+    uint64_t pol;
+    if constexpr (GTS_TMA_POLICY == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    else if constexpr (GTS_TMA_POLICY == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -1190,8 +1254,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
-template <typename T, int S, int W, int R, bool kInter>
+// XG: where runs read x (0: the warp's shared X tile, 1: a feature-major copy
+// in global memory, 2: TMEM filled from that copy; see load_x).
+template <typename T, int S, int W, int R, bool kInter, int XG>
 __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal_kernel(Args a) {
+  static_assert(XG != 2 || (sizeof(T) == 4 && W == 4 && R * 64 <= 128 && !kInter), "TMEM X: 4 warps = 128 lanes");
   const int XS = x_stride<kInter, S>(a.tile_w);
   const int AS = acc_stride<kInter, S>(a.tile_w);
   const int AW = kInter ? acc_width<kInter>(S) : a.tile_w - 1;  // cells per row
@@ -1264,16 +1331,36 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   int xb[R], ab[R];
   int64_t row[R];
   bool ok[R];
-  constexpr bool kXg = xg_enabled<kInter, S>();
+  constexpr int kXg = XG;
+  static_assert((XG != 0) == xg_enabled<kInter, S>(), "X source");
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int lr = warp * ROWS + r * 32 + lane;
     const int64_t rr = row0 + r * 32 + lane;
-    xb[r] = kXg ? (int)rr : o_x + lr * XS;  // kXg: the row (the feature-major copy is padded to whole tiles)
+    // kXg = 1: the row (the feature-major copy is padded to whole tiles); 2: the row's TMEM column base
+    xb[r] = kXg == 2 ? r * 64 : kXg ? (int)rr : o_x + lr * XS;
     ab[r] = o_acc + lr * AS;
     row[r] = row0 + r * 32 + lane;
     ok[r] = row[r] < a.n_rows;
     for (int i = 0; i < AW; ++i) sT[ab[r] + i] = (T)0;
+  }
+  __shared__ uint32_t tm_base;
+  uint32_t tm_warp = 0;
+  if constexpr (kXg == 2) {
+    // 128 TMEM columns: this block's X rows, column r * 64 + f of lane (warp, lane)
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tm_base)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tm_warp = tm_base + ((uint32_t)(32 * (warp & 3)) << 16);
+    for (int f = 0; f < a.M; ++f) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) tm_st(tm_warp + r * 64 + f, X[(size_t)f * a.col_stride + row0 + r * 32 + lane]);
+    }
+    tm_wait_st();
   }
   const int M1 = a.M + 1;
   int cur_map = -1, cur_group = -1, cur_slots = 0;
@@ -1416,13 +1503,21 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
       for (int p = 0; p < c.n_paths;) {
         const int4 ph = sP[p];
         run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S), kXg, (S / 2 < kQMax ? S / 2 : kQMax)>(
-            ph, sE, tab, sT, xb, ab, X, (int)a.col_stride);
+            ph, sE, tab, sT, xb, ab, X, kXg == 2 ? (int)tm_warp : (int)a.col_stride);
         p += ph.x >> 16;
       }
       dirty = true;
     }
   }
   flush();
+  if constexpr (kXg == 2) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm_base));
+    }
+  }
 }
 
 }  // namespace nodal
