@@ -610,8 +610,10 @@ static void plan_nodal(const PathTable& tab, int S, int nt, size_t tsize, NodalP
   // (Cutting small models into ~one chunk per SM lowered the 1-row latency of
   // cal_housing-small from 23 to 18 us but cost 30 % at 2^20 rows, since runs
   // and staging get shorter; profiles/r01h.  Not adopted.)
-  // staged bytes of a chunk: element records + path headers (16 B each) + tables
-  auto path_bytes = [&](int k, int q) { return (int64_t)16 * (k + 1) + (int64_t)tsize * nodal_path_words(k, q, nt); };
+  // staged bytes of a chunk: element records (run heads only) + path headers (16 B each) + tables
+  auto path_bytes = [&](int k, int q, bool head) {
+    return (int64_t)16 * ((head ? k : 0) + 1) + (int64_t)tsize * nodal_path_words(k, q, nt);
+  };
 
   // Chunks never span groups, so every group is planned on its own (in
   // parallel) with group-local offsets; the pieces are then concatenated in
@@ -646,7 +648,11 @@ static void plan_nodal(const PathTable& tab, int S, int nt, size_t tsize, NodalP
       while (j < order.size() && (int)members.size() < kMaxChunkPaths) {
         const int64_t p = order[j];
         const int k = tab.len(p) - 1, q = (k + 1) / 2;
-        const int64_t w = path_bytes(k, q);
+        // a path repeating its predecessor's feature set joins its run (no element
+        // records); sorting the chunk below only merges runs further, so this
+        // count bounds the staged bytes
+        const bool head = members.empty() || !same_set(members.back(), p);
+        const int64_t w = path_bytes(k, q, head);
         if (!members.empty() && bytes + w > chunk_bytes) break;
         if (!identity) {  // union of two sorted feature lists
           const int32_t* pf = &tab.feature[tab.path_offset[p] + 1];
@@ -664,7 +670,6 @@ static void plan_nodal(const PathTable& tab, int S, int nt, size_t tsize, NodalP
         }
         members.push_back(p);
         bytes += w;
-        nel += k;
         ++j;
       }
       if (identity) {
@@ -685,7 +690,6 @@ static void plan_nodal(const PathTable& tab, int S, int nt, size_t tsize, NodalP
       c.map_id = map_id;
       c.n_slots = (int32_t)nf;
       c.n_paths = (int32_t)members.size();
-      c.n_elems = (int32_t)nel;
       int32_t table = 0, rel = 0, maxq = 0;
       double ws = 0, wi = 0;
       size_t run_head = 0;
@@ -699,20 +703,27 @@ static void plan_nodal(const PathTable& tab, int S, int nt, size_t tsize, NodalP
         if (run_head == mi) pr.k |= 1 << 16;
         else pt.paths[head_index].k += 1 << 16;
         pr.q = q;
-        pr.elem = rel;
+        // element records: run heads only; the run's other paths share them
+        // (same features, so the same x values and tile slots; each path's
+        // split bounds are in its own rho rows)
+        pr.elem = run_head == mi ? rel : pt.paths[head_index].elem;
         pr.table = table;
         pr.src = p;
         pt.paths.push_back(pr);
-        for (int64_t e = tab.path_offset[p] + 1; e < tab.path_offset[p + 1]; ++e) {
-          const int32_t f = tab.feature[e];
-          pt.slots.push_back((uint8_t)(identity ? f : (std::lower_bound(feats, feats + nf, f) - feats)));
+        if (run_head == mi) {
+          for (int64_t e = tab.path_offset[p] + 1; e < tab.path_offset[p + 1]; ++e) {
+            const int32_t f = tab.feature[e];
+            pt.slots.push_back((uint8_t)(identity ? f : (std::lower_bound(feats, feats + nf, f) - feats)));
+          }
+          rel += k;
         }
-        rel += k;
         table += nodal_path_words(k, q, nt);
         maxq = std::max(maxq, q);
         ws += nodal_shap_flops(k, q);
         wi += nodal_inter_flops(k, q);
       }
+      nel = rel;
+      c.n_elems = (int32_t)nel;
       c.table_words = table;
       c.max_q = maxq;
       c.data_bytes = (int32_t)(16 * ((int64_t)nel + c.n_paths) + (int64_t)tsize * table);
@@ -1000,7 +1011,7 @@ static void write_region(const PathTable& tab, const NodalPlan& np, const GaussT
     const int k = pr.k & 0xff, Q = pr.q, QP = nodal_qp(Q), RW = nodal_rw(Q), ES = nodal_es(Q, nt), BO = nodal_bo(Q);
     const int64_t e0 = tab.path_offset[pr.src] + 1;  // first non-root element
     const uint8_t* sl = &np.slots[c.elem_begin + pr.elem];
-    for (int s = 0; s < k; ++s) {
+    for (int s = 0; s < ((pr.k >> 16) != 0 ? k : 0); ++s) {  // run heads write the run's records
       int32_t* rec = E + 4 * (int64_t)(pr.elem + s);
       std::memcpy(&rec[0], &tab.lower[e0 + s], 4);
       std::memcpy(&rec[1], &tab.upper[e0 + s], 4);

@@ -491,12 +491,12 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
   for (int r = 0; r < R; ++r) om[r] = 0u;
 #pragma unroll 1
   for (int s = 0; s < k; ++s) {
-    const int4 rec = E[s];
-    T rho[Q];
-    lds_vec(rho, tab + Lay<Q, NT>::rho(s));
+    const int4 rec = E[s];  // the run head's record: x source
+    T rho[Q], lo, hi;
+    lds_rho(rho, lo, hi, tab + Lay<Q, NT>::rho(s));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool o = one_fraction(load_x<T, NT, kXg>(sT, xb[r], rec, xg, cs), rec);
+      const bool o = in_bounds(load_x<T, NT, kXg>(sT, xb[r], rec, xg, cs), lo, hi);
       om[r] |= (uint32_t)o << s;
       if (!o) {
 #pragma unroll
@@ -552,12 +552,12 @@ __device__ __forceinline__ void inter_extend(int k, const int4* __restrict__ E, 
 #pragma unroll
   for (int r = 0; r < R; ++r) om[r] = 0u;
   auto body = [&](int s) {
-    const int4 rec = E[s];
-    T rho[Q];
-    lds_vec(rho, tp + Lay<Q, 3>::rho(s));
+    const int4 rec = E[s];  // the run head's record: x source
+    T rho[Q], lo, hi;
+    lds_rho(rho, lo, hi, tp + Lay<Q, 3>::rho(s));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool o = one_fraction(sT[xb[r] + rec.z], rec);
+      const bool o = in_bounds(sT[xb[r] + rec.z], lo, hi);
       om[r] |= (uint32_t)o << s;
       if (!o) {
 #pragma unroll
@@ -995,7 +995,7 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
-#define GTS_DYN(QQ) case QQ: if constexpr (QQ <= QM) shap_path_dyn<T, QQ, 1, NT, kXg>(k, E + p * k, tab + p * words, xb1, ab1, xg, cs); break;
+#define GTS_DYN(QQ) case QQ: if constexpr (QQ <= QM) shap_path_dyn<T, QQ, 1, NT, kXg>(k, E, tab + p * words, xb1, ab1, xg, cs); break;
                   GTS_DYN(9) GTS_DYN(10) GTS_DYN(11) GTS_DYN(12) GTS_DYN(13) GTS_DYN(14) GTS_DYN(15) GTS_DYN(16)
 #undef GTS_DYN
                   default: break;
@@ -1020,7 +1020,7 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
-#define GTS_DYN(QQ) case QQ: if constexpr (QQ <= QM) shap_path_dyn<T, QQ, 1, NT, kXg>(k, E + p * k, tab + p * words, xb1, ab1, xg, cs); break;
+#define GTS_DYN(QQ) case QQ: if constexpr (QQ <= QM) shap_path_dyn<T, QQ, 1, NT, kXg>(k, E, tab + p * words, xb1, ab1, xg, cs); break;
                   GTS_DYN(9) GTS_DYN(10) GTS_DYN(11) GTS_DYN(12) GTS_DYN(13) GTS_DYN(14) GTS_DYN(15) GTS_DYN(16)
 #undef GTS_DYN
                   default: break;
@@ -1079,7 +1079,7 @@ __device__ __forceinline__ void run_dispatch(int4 ph, const int4* __restrict__ E
             default:
               for (int p = 0; p < n_run; ++p) {
                 switch (q) {
-#define GTS_IP(QQ) case QQ: if constexpr (QQ <= QM) inter_path<T, QQ, 1, false>(k, E + p * k, tab + p * words, gam, xb1, ab1); break;
+#define GTS_IP(QQ) case QQ: if constexpr (QQ <= QM) inter_path<T, QQ, 1, false>(k, E, tab + p * words, gam, xb1, ab1); break;
                   GTS_IP(6) GTS_IP(7) GTS_IP(8) GTS_IP(9) GTS_IP(10) GTS_IP(11) GTS_IP(12) GTS_IP(13)
                   GTS_IP(14) GTS_IP(15) GTS_IP(16)
 #undef GTS_IP

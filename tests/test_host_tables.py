@@ -149,7 +149,8 @@ def test_nodal_blob_invariants(name, slots):
     for q in range(view["n_paths"]):
         a, bb = view["path_offset"][q] + 1, view["path_offset"][q + 1]
         if bb > a:
-            ref.setdefault(tuple(view["feature"][a:bb]), []).append((float(view["v"][q]), view["zero_fraction"][a:bb]))
+            ref.setdefault(tuple(view["feature"][a:bb]), []).append(
+                (float(view["v"][q]), view["zero_fraction"][a:bb], view["lower"][a:bb], view["upper"][a:bb]))
     nt = 2 if hd["S"] > 16 else 3  # SHAP-only blobs drop h and alpha (blob_format.h)
 
     def slot_of(el):
@@ -158,6 +159,7 @@ def test_nodal_blob_invariants(name, slots):
 
     seen = 0
     for c in chunks:
+        n_rec = 0
         mp = smap[c["slotmap_begin"]:c["slotmap_begin"] + c["n_slots"]]
         assert np.all(np.diff(mp) > 0) and c["n_slots"] <= hd["S"]
         reg = blob[c["data_off"]:c["data_off"] + c["data_bytes"]]
@@ -188,7 +190,7 @@ def test_nodal_blob_invariants(name, slots):
                 v = float(-d[0] * (1 - t[0]) / wq[0])
                 cands = ref[feats]
                 best = min(range(len(cands)), key=lambda ii: abs(cands[ii][0] - v))
-                v, z = cands.pop(best)
+                v, z, plo, phi_ = cands.pop(best)
                 A = z[:, None] + (1 - z[:, None]) * t[None]
                 B = z[:, None] * (1 - t[None])
                 np.testing.assert_allclose(tab[t0:t0 + Q], A.prod(axis=0), rtol=1e-12)
@@ -207,12 +209,14 @@ def test_nodal_blob_invariants(name, slots):
                                            rtol=1e-12, atol=1e-300)
                 if nt == 3:
                     np.testing.assert_allclose(rows[:, RW + QP:RW + QP + Q], (1 - z[:, None]) / A, rtol=1e-12, atol=1e-300)
-                lo = E[e0:e0 + k, 0].view(np.float32)
-                hi = E[e0:e0 + k, 1].view(np.float32)
-                assert np.all(lo == lo)  # bounds stored as fp32 bit patterns
-                # the rho row carries the same bounds (as T) for EXTEND's o_s
-                np.testing.assert_array_equal(rows[:, BO], lo.astype(np.float64))
-                np.testing.assert_array_equal(rows[:, BO + 1], hi.astype(np.float64))
+                # the rho rows carry the path's own split bounds (as T) for EXTEND's o_s
+                np.testing.assert_array_equal(rows[:, BO], np.asarray(plo, np.float32).astype(np.float64))
+                np.testing.assert_array_equal(rows[:, BO + 1], np.asarray(phi_, np.float32).astype(np.float64))
+                # element records: the run head's (every path of a run points at them)
+                assert e0 == P[i, 2]
+                if j == 0:
+                    n_rec += k
                 seen += 1
             i += run
+        assert n_rec == c["n_elems"]  # records of run heads only
     assert seen == hd["n_kept_paths"] and not any(ref.values())
