@@ -86,18 +86,20 @@ struct PathRec {
 // Nodal table of one path (T words, shared memory; NT rows per record, the
 // third row only when NT = 3; interaction blobs always have NT = 3, SHAP-only
 // blobs NT = nodal_tables(S)).  Rows are padded to QP = round_up(Q, 4) words
-// (16-byte vector loads), except the rho row of an element, which also carries
-// the element's split bounds: RW = nodal_rw(Q) words, lower / upper (as T) at
-// words BO = nodal_bo(Q) and BO + 1, after the (paired, zero-padded) nodes.  So
-// EXTEND reads one row per element and path (no element record): for Q = 1, 2,
-// 5, 6 the bounds sit in the row's padding (one 16-byte load less per element),
-// for Q = 3, 4, 7, 8 they take one 8-byte load instead of the record's 16-byte
-// one.  With A_sq = z_s + (1-z_s) t_q, B_sq = z_s (1 - t_q) (f_s(t_q) for o_s = 1 / 0):
+// (16-byte vector loads).  Every path carries its own split bounds (as T), so
+// EXTEND needs no element record (those are stored for run heads only): when
+// Q mod 4 is 1 or 2 (nodal_inrow) the rho row has room for them after its
+// zero-padded node pairs -- RW = nodal_rw(Q) words, lower / upper at BO =
+// nodal_bo(Q) -- so they cost no load at all; otherwise (the rows are full)
+// they form a block {lower_s, upper_s} x 2Q after the path rows (one 16-byte
+// load per two elements in fp32).  With A_sq = z_s + (1-z_s) t_q,
+// B_sq = z_s (1 - t_q) (f_s(t_q) for o_s = 1 / 0):
 //   c[QP]  prod_s A_sq                  (P(t_q) when every o = 1)
 //   d[QP]  -v w_q / (1 - t_q)           (SHAP: phi of every o = 0 element, times P_q)
 //   h[QP]  v w_q / 2                    (interactions: W_q = h_q P_q)
+//   [bounds block, nodal_bw(Q) words: lower_s, upper_s for s < k]
 //   per element s (stride nodal_es(Q, NT) words):
-//     rho[RW]   = B_sq / A_sq, then lower_s, upper_s at BO  (EXTEND of an o = 0 element; o_s)
+//     rho[RW]   = B_sq / A_sq [, then lower_s, upper_s at BO]  (EXTEND of an o = 0 element; o_s)
 //     C'[QP]    = v w_q ((1 - z_s)/A_sq + 1/(1 - t_q))   (SHAP: C_sq - d_q, where
 //               C_sq = v w_q (1-z_s)/A_sq gives phi_s = sum_q P_q C_sq when o_s = 1)
 //     alpha[QP] = (1 - z_s) / A_sq      (interactions: u_sq when o_s = 1)
@@ -107,10 +109,14 @@ GTS_HD constexpr int nodal_qp(int q) { return (q + 3) & ~3; }
 // row ({c, d} and {rho, C'} per element) instead of 3 -- 1.5x more paths per
 // 16 KB chunk, hence fewer slot-map gathers and flushes for wide models.
 GTS_HD constexpr int nodal_tables(int slots) { return slots > 16 ? 2 : 3; }
-GTS_HD constexpr int nodal_bo(int q) { return (q + 1) & ~1; }               // bounds offset in the rho row
-GTS_HD constexpr int nodal_rw(int q) { return (nodal_bo(q) + 2 + 3) & ~3; }  // rho row width
+GTS_HD constexpr bool nodal_inrow(int q) { return (q & 3) == 1 || (q & 3) == 2; }  // bounds in the rho row's padding
+GTS_HD constexpr int nodal_bo(int q) { return (q + 1) & ~1; }  // in-row: bounds offset in the rho row
+GTS_HD constexpr int nodal_rw(int q) { return nodal_inrow(q) ? (nodal_bo(q) + 2 + 3) & ~3 : nodal_qp(q); }  // rho row
+GTS_HD constexpr int nodal_bw(int q) { return nodal_inrow(q) ? 0 : 4 * q; }  // bounds block: {lo, hi} x (k <= 2Q)
 GTS_HD constexpr int nodal_es(int q, int nt = 3) { return nodal_rw(q) + (nt - 1) * nodal_qp(q); }  // element stride
-GTS_HD constexpr int nodal_path_words(int k, int q, int nt = 3) { return nt * nodal_qp(q) + k * nodal_es(q, nt); }
+GTS_HD constexpr int nodal_path_words(int k, int q, int nt = 3) {
+  return nt * nodal_qp(q) + nodal_bw(q) + k * nodal_es(q, nt);
+}
 
 // WARP_BINS lane arrays (each [n_bins * 32], in this order after off_elems):
 //   int32 feature   (-1 root lane, -2 empty lane)

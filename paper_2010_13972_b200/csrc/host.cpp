@@ -1008,7 +1008,8 @@ static void write_region(const PathTable& tab, const NodalPlan& np, const GaussT
     Pp[4 * p + 1] = pr.q;
     Pp[4 * p + 2] = pr.elem;
     Pp[4 * p + 3] = pr.table;
-    const int k = pr.k & 0xff, Q = pr.q, QP = nodal_qp(Q), RW = nodal_rw(Q), ES = nodal_es(Q, nt), BO = nodal_bo(Q);
+    const int k = pr.k & 0xff, Q = pr.q, QP = nodal_qp(Q), RW = nodal_rw(Q), ES = nodal_es(Q, nt), BO = nodal_bo(Q),
+              BW = nodal_bw(Q);
     const int64_t e0 = tab.path_offset[pr.src] + 1;  // first non-root element
     const uint8_t* sl = &np.slots[c.elem_begin + pr.elem];
     for (int s = 0; s < ((pr.k >> 16) != 0 ? k : 0); ++s) {  // run heads write the run's records
@@ -1034,16 +1035,16 @@ static void write_region(const PathTable& tab, const NodalPlan& np, const GaussT
       for (int s = 0; s < k; ++s) {
         const double zs = z[s];
         const double A = zs + (1.0 - zs) * tt, iA = 1.0 / A;
-        T* row = t + nt * QP + s * ES;
+        T* row = t + nt * QP + BW + s * ES;
         row[q] = (T)(zs * (1.0 - tt) * iA);                 // rho = B / A
         row[RW + q] = (T)(v * w * ((1.0 - zs) * iA + r1));  // C' = C - d
         if (nt == 3) row[RW + QP + q] = (T)((1.0 - zs) * iA);
       }
     }
-    for (int s = 0; s < k; ++s) {  // split bounds in the rho row (exact in T: they are fp32 values)
-      T* row = t + nt * QP + s * ES;
-      row[BO] = (T)tab.lower[e0 + s];
-      row[BO + 1] = (T)tab.upper[e0 + s];
+    for (int s = 0; s < k; ++s) {  // split bounds (exact in T: they are fp32 values)
+      T* b = nodal_inrow(Q) ? t + nt * QP + s * ES + BO : t + nt * QP + 2 * s;
+      b[0] = (T)tab.lower[e0 + s];
+      b[1] = (T)tab.upper[e0 + s];
     }
   }
 }

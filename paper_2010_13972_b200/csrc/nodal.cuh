@@ -117,12 +117,25 @@ __device__ __forceinline__ void lds_pairs(float2 (&dst)[N], const float* src) {
 // (interactions; NT = 3).
 template <int Q, int NT>
 struct Lay {
-  static constexpr int QP = (Q + 3) & ~3, BO = (Q + 1) & ~1, RW = (BO + 2 + 3) & ~3, ES = RW + (NT - 1) * QP;
-  static_assert(BO == nodal_bo(Q) && RW == nodal_rw(Q) && ES == nodal_es(Q, NT), "table layout");
-  __device__ static __forceinline__ int rho(int s) { return NT * QP + s * ES; }
-  __device__ static __forceinline__ int cp(int s) { return NT * QP + s * ES + RW; }
-  __device__ static __forceinline__ int al(int s) { return NT * QP + s * ES + RW + QP; }
+  static constexpr bool kInRow = (Q & 3) == 1 || (Q & 3) == 2;
+  static constexpr int QP = (Q + 3) & ~3, BO = (Q + 1) & ~1, RW = kInRow ? (BO + 2 + 3) & ~3 : QP,
+                       BW = kInRow ? 0 : 4 * Q, ES = RW + (NT - 1) * QP;
+  static_assert(kInRow == nodal_inrow(Q) && BO == nodal_bo(Q) && RW == nodal_rw(Q) && BW == nodal_bw(Q) &&
+                    ES == nodal_es(Q, NT),
+                "table layout");
+  __device__ static __forceinline__ int bnd(int s) { return NT * QP + 2 * s; }  // bounds block (!kInRow)
+  __device__ static __forceinline__ int rho(int s) { return NT * QP + BW + s * ES; }
+  __device__ static __forceinline__ int cp(int s) { return rho(s) + RW; }
+  __device__ static __forceinline__ int al(int s) { return rho(s) + RW + QP; }
 };
+
+// 16 bytes of bounds: two fp32 elements' {lo, hi} or one fp64 element's
+template <typename T>
+struct BQ;
+template <>
+struct BQ<float> { using type = float4; };
+template <>
+struct BQ<double> { using type = double2; };
 
 // The first NW words of a 16-byte aligned row by 16-byte loads (an 8-byte
 // load for a trailing pair of fp32 words).
@@ -148,28 +161,55 @@ __device__ __forceinline__ void lds_words(T (&w)[NW], const T* src) {
   }
 }
 
-// rho_s at the Q nodes and the split bounds of element s, from its rho row.
-template <typename T, int Q>
-__device__ __forceinline__ void lds_rho(T (&rho)[Q], T& lo, T& hi, const T* row) {
-  constexpr int BO = (Q + 1) & ~1;
-  T w[BO + 2];
-  lds_words(w, row);
+// The split bounds of element s from the bounds block (fp32: one 16-byte load
+// for elements s, s + 1, kept in bq -- callers walk s upwards from 0).
+template <typename T, int Q, int NT>
+__device__ __forceinline__ void lds_bounds(T& lo, T& hi, const T* tp, int s, typename BQ<T>::type& bq) {
+  using L = Lay<Q, NT>;
+  if constexpr (sizeof(T) == 4) {
+    if ((s & 1) == 0) bq = *reinterpret_cast<const float4*>(tp + L::bnd(s));
+    lo = (s & 1) ? bq.z : bq.x;
+    hi = (s & 1) ? bq.w : bq.y;
+  } else {
+    bq = *reinterpret_cast<const double2*>(tp + L::bnd(s));
+    lo = bq.x;
+    hi = bq.y;
+  }
+}
+
+// rho_s at the Q nodes and the split bounds of element s of the path table at tp.
+template <typename T, int Q, int NT>
+__device__ __forceinline__ void lds_rho(T (&rho)[Q], T& lo, T& hi, const T* tp, int s, typename BQ<T>::type& bq) {
+  using L = Lay<Q, NT>;
+  if constexpr (L::kInRow) {
+    T w[L::BO + 2];
+    lds_words(w, tp + L::rho(s));
 #pragma unroll
-  for (int q = 0; q < Q; ++q) rho[q] = w[q];
-  lo = w[BO];
-  hi = w[BO + 1];
+    for (int q = 0; q < Q; ++q) rho[q] = w[q];
+    lo = w[L::BO];
+    hi = w[L::BO + 1];
+  } else {
+    lds_vec(rho, tp + L::rho(s));
+    lds_bounds<T, Q, NT>(lo, hi, tp, s, bq);
+  }
 }
 
 // fp32: rho_s on packed node pairs (odd Q: the zero pad completes the last pair) and the bounds.
-template <int Q>
-__device__ __forceinline__ void lds_rho_pairs(float2 (&rh)[(Q + 1) / 2], float& lo, float& hi, const float* row) {
-  constexpr int BO = (Q + 1) & ~1;
-  float w[BO + 2];
-  lds_words(w, row);
+template <int Q, int NT>
+__device__ __forceinline__ void lds_rho_pairs(float2 (&rh)[(Q + 1) / 2], float& lo, float& hi, const float* tp, int s,
+                                              float4& bq) {
+  using L = Lay<Q, NT>;
+  if constexpr (L::kInRow) {
+    float w[L::BO + 2];
+    lds_words(w, tp + L::rho(s));
 #pragma unroll
-  for (int h = 0; h < (Q + 1) / 2; ++h) rh[h] = make_float2(w[2 * h], w[2 * h + 1]);
-  lo = w[BO];
-  hi = w[BO + 1];
+    for (int h = 0; h < (Q + 1) / 2; ++h) rh[h] = make_float2(w[2 * h], w[2 * h + 1]);
+    lo = w[L::BO];
+    hi = w[L::BO + 1];
+  } else {
+    lds_pairs(rh, tp + L::rho(s));
+    lds_bounds<float, Q, NT>(lo, hi, tp, s, bq);
+  }
 }
 
 template <typename T>
@@ -286,11 +326,12 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
     uint32_t om[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) om[r] = 0u;
+    typename BQ<T>::type bq;
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
         T rho[Q], lo, hi;
-        lds_rho(rho, lo, hi, tp + L::rho(s));
+        lds_rho<T, Q, NT>(rho, lo, hi, tp, s, bq);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool o = in_bounds(xv[r][s], lo, hi);
@@ -406,12 +447,13 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
     uint32_t om[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) om[r] = 0u;
+    float4 bq;
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
         float2 rh[QH];
         float lo, hi;
-        lds_rho_pairs<Q>(rh, lo, hi, tp + L::rho(s));
+        lds_rho_pairs<Q, NT>(rh, lo, hi, tp, s, bq);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool o = in_bounds(xv[r][s], lo, hi);
@@ -489,11 +531,12 @@ __device__ __forceinline__ void shap_path_dyn(int k, const int4* __restrict__ E,
   uint32_t om[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) om[r] = 0u;
+  typename BQ<T>::type bq;
 #pragma unroll 1
   for (int s = 0; s < k; ++s) {
     const int4 rec = E[s];  // the run head's record: x source
     T rho[Q], lo, hi;
-    lds_rho(rho, lo, hi, tab + Lay<Q, NT>::rho(s));
+    lds_rho<T, Q, NT>(rho, lo, hi, tab, s, bq);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool o = in_bounds(load_x<T, NT, kXg>(sT, xb[r], rec, xg, cs), lo, hi);
@@ -551,10 +594,11 @@ __device__ __forceinline__ void inter_extend(int k, const int4* __restrict__ E, 
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) om[r] = 0u;
+  typename BQ<T>::type bq;
   auto body = [&](int s) {
     const int4 rec = E[s];  // the run head's record: x source
     T rho[Q], lo, hi;
-    lds_rho(rho, lo, hi, tp + Lay<Q, 3>::rho(s));
+    lds_rho<T, Q, 3>(rho, lo, hi, tp, s, bq);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool o = in_bounds(sT[xb[r] + rec.z], lo, hi);
@@ -620,11 +664,12 @@ __device__ __forceinline__ void inter_run(int k, int n_run, const int4* __restri
         for (int q = 0; q < Q; ++q) P[r][q] = c0[q];
       }
     }
+    typename BQ<T>::type bq;
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
         T rho[Q], lo, hi;
-        lds_rho(rho, lo, hi, tp + L::rho(s));
+        lds_rho<T, Q, 3>(rho, lo, hi, tp, s, bq);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool o = in_bounds(xv[r][s], lo, hi);
@@ -812,12 +857,13 @@ __device__ __forceinline__ void inter_run_q2(int k, int n_run, const int4* __res
     for (int h = 0; h < NP; ++h) P[h] = tp[h];
     float Pt = kTail ? tf[TQ] : 0.f;
     uint32_t om = 0u;
+    float4 bq;
 #pragma unroll
     for (int s = 0; s < KM; ++s) {
       if (s < KM - 1 || s < k) {
-        float w[L::BO + 2];
-        lds_words(w, tf + L::rho(s));
-        const bool o = in_bounds(xv[s], w[L::BO], w[L::BO + 1]);
+        float w[Q], lo, hi;
+        lds_rho<float, Q, 3>(w, lo, hi, tf, s, bq);
+        const bool o = in_bounds(xv[s], lo, hi);
         om |= (uint32_t)o << s;
         if (!o) {
 #pragma unroll

@@ -197,21 +197,25 @@ def test_nodal_blob_invariants(name, slots):
                 np.testing.assert_allclose(tab[t0 + QP:t0 + QP + Q], -v * wq / (1 - t), rtol=1e-12, atol=1e-300)
                 if nt == 3:
                     np.testing.assert_allclose(tab[t0 + 2 * QP:t0 + 2 * QP + Q], 0.5 * v * wq, rtol=1e-12, atol=1e-300)
-                # element rows (blob_format.h): rho[RW] with the bounds at BO, C'[QP] (, alpha[QP])
+                # element rows (blob_format.h): rho[RW] (with the bounds at BO when Q mod 4 is 1 or 2),
+                # C'[QP] (, alpha[QP]); otherwise the bounds form a block of 2 x 2Q words after the path rows
+                inrow = (Q & 3) in (1, 2)
                 BO = (Q + 1) & ~1
-                RW = (BO + 2 + 3) & ~3
+                RW = (BO + 2 + 3) & ~3 if inrow else QP
+                BW = 0 if inrow else 4 * Q
                 ES = RW + (nt - 1) * QP
-                rows = tab[t0 + nt * QP:t0 + nt * QP + k * ES].reshape(k, ES)
+                rows = tab[t0 + nt * QP + BW:t0 + nt * QP + BW + k * ES].reshape(k, ES)
+                bounds = rows[:, BO:BO + 2] if inrow else tab[t0 + nt * QP:t0 + nt * QP + 2 * k].reshape(k, 2)
                 np.testing.assert_allclose(rows[:, :Q], B / A, rtol=1e-12)
-                assert np.all(rows[:, Q:BO] == 0)  # the zero pad of an odd Q's last node pair
+                assert np.all(rows[:, Q:(BO if inrow else RW)] == 0)  # the zero pad of the node pairs
                 # C' = C - d: the SHAP constant with the o = 0 share folded out (nodal.cuh shap_run)
                 np.testing.assert_allclose(rows[:, RW:RW + Q], v * wq[None] * ((1 - z[:, None]) / A + 1 / (1 - t[None])),
                                            rtol=1e-12, atol=1e-300)
                 if nt == 3:
                     np.testing.assert_allclose(rows[:, RW + QP:RW + QP + Q], (1 - z[:, None]) / A, rtol=1e-12, atol=1e-300)
                 # the rho rows carry the path's own split bounds (as T) for EXTEND's o_s
-                np.testing.assert_array_equal(rows[:, BO], np.asarray(plo, np.float32).astype(np.float64))
-                np.testing.assert_array_equal(rows[:, BO + 1], np.asarray(phi_, np.float32).astype(np.float64))
+                np.testing.assert_array_equal(bounds[:, 0], np.asarray(plo, np.float32).astype(np.float64))
+                np.testing.assert_array_equal(bounds[:, 1], np.asarray(phi_, np.float32).astype(np.float64))
                 # element records: the run head's (every path of a run points at them)
                 assert e0 == P[i, 2]
                 if j == 0:
