@@ -104,6 +104,13 @@ struct PathRec {
 //               C_sq = v w_q (1-z_s)/A_sq gives phi_s = sum_q P_q C_sq when o_s = 1)
 //     alpha[QP] = (1 - z_s) / A_sq      (interactions: u_sq when o_s = 1)
 GTS_HD constexpr int nodal_qp(int q) { return (q + 3) & ~3; }
+// Algorithmic FP operations of one (row, path) with k non-root elements and
+// Q = ceil(k/2) nodes (also the split-balancing work).
+GTS_HD constexpr double nodal_shap_flops(int k, int q) { return 3.0 * k * q + 3.0 * k + 2.0 * q; }
+GTS_HD constexpr double nodal_inter_flops(int k, int q) {
+  // EXTEND kQ, W Q, y kQ, phi_i kQ + k, pairs k(k-1)/2 * 2Q, cell adds k(k-1)/2 + k, compares 2k
+  return (double)k * (k - 1) * q + 3.0 * k * q + q + 4.0 * k + 0.5 * k * (k - 1);
+}
 // Blobs with more than 16 slots serve only the SHAP kernel (the interaction
 // kernel takes 8 or 16 slots), so they drop h and alpha: NT = 2 tables per
 // row ({c, d} and {rho, C'} per element) instead of 3 -- 1.5x more paths per

@@ -549,11 +549,6 @@ static int pick_slots(int32_t requested, int32_t M) {
 }
 
 // nodal op counts per (row, path), DESIGN.md §6
-static double nodal_shap_flops(int k, int q) { return 3.0 * k * q + 3.0 * k + 2.0 * q; }
-static double nodal_inter_flops(int k, int q) {
-  // EXTEND kQ, W Q, y kQ, phi_i kQ + k, pairs k(k-1)/2 * 2Q, cell adds k(k-1)/2 + k, compares 2k
-  return (double)k * (k - 1) * q + 3.0 * k * q + q + 4.0 * k + 0.5 * k * (k - 1);
-}
 static double paper_shap_flops(int k) { return 5.5 * k * k + 7.5 * k; }
 static double paper_inter_flops(int k) { return paper_shap_flops(k) + (double)k * (k - 1) * (5.5 * k + 1) + 2.0 * k; }
 

@@ -1148,6 +1148,11 @@ struct Args {
   void* out;
   void* out_phi;  // interaction kernel only: if set, the phi_i cells are also added to phi (fused call)
   int upper_only;  // interaction kernel only: write cells (i, j) with i < j only; mirror_kernel fills (j, i)
+  // interaction kernel only: the W warps of a block share one row tile (32 R
+  // rows) and split each chunk's runs by work; their tiles are folded at each
+  // flush.  Wide models: a block's phi_ij rows shrink W-fold, so the rows in
+  // flight of all resident blocks stay in L2 and the flush REDs hit it.
+  int shared_rows;
   int n_splits;
   // Block decomposition: blockIdx = ((batch * n_bgroups + g) * tiles_per_batch + tile) * n_splits + split.
   // n_bgroups = 1: a block walks the chunks of every group (its split of them);
@@ -1331,8 +1336,10 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   const int64_t batch = bg / a.n_bgroups;
   const int bgroup = (int)(bg % a.n_bgroups);
   const int64_t row_tile = batch * a.tiles_per_batch + tile;
-  const int64_t row0 = row_tile * (W * ROWS) + (int64_t)warp * ROWS;
-  if (row_tile * (W * ROWS) >= a.n_rows) return;  // padding tile of the last batch (uniform per block)
+  const bool shared_rows = kInter && a.shared_rows != 0;  // block-uniform
+  const int64_t rows_per_block = shared_rows ? ROWS : W * ROWS;
+  const int64_t row0 = row_tile * rows_per_block + (shared_rows ? 0 : (int64_t)warp * ROWS);
+  if (row_tile * rows_per_block >= a.n_rows) return;  // padding tile of the last batch (uniform per block)
 
   // this block's chunk range: all chunks, or group bgroup's (chunks are in group order)
   int64_t g_lo = 0, g_hi = a.n_chunks;
@@ -1418,7 +1425,67 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   // row (coalesced RED) and the loads of the tile are independent (ILP).  One
   // atomic per non-zero (row, group, feature) cell.
   const int tile_row0 = warp * ROWS;
+  // Shared-rows flush (interactions): fold the W warps' tiles into warp 0's,
+  // then warp w flushes the slot rows i = w mod W of it, lane = row; the Eq. 6
+  // diagonal of slot i reads its whole row sum (cells (i, j > i) and (j < i, i)).
+  auto flush_shared = [&]() {
+    if constexpr (kInter) {
+      __syncthreads();
+      const int cells = ROWS * AS;
+      T* const t0 = sT + o_acc;
+      for (int i = tid; i < cells; i += W * 32) {
+        T v = t0[i];
+#pragma unroll
+        for (int w = 1; w < W; ++w) {
+          v += t0[w * cells + i];
+          t0[w * cells + i] = (T)0;
+        }
+        t0[i] = v;
+      }
+      __syncthreads();
+      int fm[S];
+#pragma unroll
+      for (int j = 0; j < S; ++j) fm[j] = j < cur_slots ? __ldg(slotmap + cur_map_begin + j) : 0;
+#pragma unroll 1
+      for (int r = 0; r < R; ++r) {
+        const int64_t rg = row0 + r * 32 + lane;
+        const bool ok_r = rg < a.n_rows;
+        const T* const tl = t0 + (r * 32 + lane) * AS;
+        T* const base = out + ((size_t)(ok_r ? rg : 0) * a.G + cur_group) * (size_t)M1 * M1;
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          if (i < cur_slots && (i % W) == warp) {
+            T rs = (T)0;
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+              if (j != i && j < cur_slots) {
+                const int c = j > i ? i * (2 * S - i - 1) / 2 + j : j * (2 * S - j - 1) / 2 + i;
+                const T v = tl[c];
+                rs += v;
+                if (j > i && ok_r && v != (T)0) {
+                  atomicAdd(base + (size_t)fm[i] * M1 + fm[j], v);
+                  if (!a.upper_only) atomicAdd(base + (size_t)fm[j] * M1 + fm[i], v);
+                }
+              }
+            }
+            const T di = tl[i * (2 * S - i - 1) / 2 + i];  // Eq. 6: phi_ii = phi_i - sum_{j != i} phi_ij
+            const T d = di - rs;
+            if (ok_r && d != (T)0) atomicAdd(base + (size_t)fm[i] * (M1 + 1), d);
+            if (ok_r && a.out_phi != nullptr && di != (T)0)
+              atomicAdd(static_cast<T*>(a.out_phi) + ((size_t)rg * a.G + cur_group) * M1 + fm[i], di);
+          }
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < cells; i += W * 32) t0[i] = (T)0;
+    }
+  };
   auto flush = [&]() {
+    if (shared_rows) {
+      if (dirty) flush_shared();
+      dirty = false;
+      return;
+    }
     if (dirty) {
       __syncwarp();
       if constexpr (kInter) {
@@ -1546,10 +1613,20 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
       const int4* sE = reinterpret_cast<const int4*>(stage0 + b * buf_bytes);
       const int4* sP = sE + c.n_elems;
       const T* tab = reinterpret_cast<const T*>(sP + c.n_paths);
+      // shared rows: warp w takes the runs whose work midpoint falls in its W-th of the chunk's work
+      const double cw = shared_rows ? work[ci + 1] - work[ci] : 0.0;
+      double cum = 0.0;
       for (int p = 0; p < c.n_paths;) {
         const int4 ph = sP[p];
-        run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S), kXg, (S / 2 < kQMax ? S / 2 : kQMax)>(
-            ph, sE, tab, sT, xb, ab, X, kXg == 2 ? (int)tm_warp : (int)a.col_stride);
+        bool mine = true;
+        if (shared_rows) {
+          const double wr = (ph.x >> 16) * nodal_inter_flops(ph.x & 0xff, ph.y);
+          mine = min(W - 1, (int)((double)W * (cum + 0.5 * wr) / cw)) == warp;
+          cum += wr;
+        }
+        if (mine)
+          run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S), kXg, (S / 2 < kQMax ? S / 2 : kQMax)>(
+              ph, sE, tab, sT, xb, ab, X, kXg == 2 ? (int)tm_warp : (int)a.col_stride);
         p += ph.x >> 16;
       }
       dirty = true;
