@@ -269,21 +269,7 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   per_sm = std::max(per_sm, 1);
-  // Interactions on wide models (per-chunk maps, mirror pass): when the phi_ij
-  // rows of one group for a block's W row tiles exceed 1/8 of the L2 budget,
-  // the W warps share one row tile (Args::shared_rows).  GTS_INTER_SHARED_ROWS
-  // = 0 / 2 in the environment forces it off / on (tests).
-  bool shared_rows = false;
-  if constexpr (kInter) {
-    const int64_t M1s = info->n_features + 1;
-    shared_rows = uses_mirror(info) &&
-                  (int64_t)W * 32 * R * M1s * M1s * (int64_t)sizeof(T) > ((int64_t)GTS_L2_BUDGET_MB << 20) / 8;
-    if (const char* e = getenv("GTS_INTER_SHARED_ROWS")) {
-      if (e[0] == '0') shared_rows = false;
-      if (e[0] == '2') shared_rows = W > 1;
-    }
-  }
-  const int64_t rows_per_block = (shared_rows ? 1 : (int64_t)W) * 32 * R;
+  const int64_t rows_per_block = (int64_t)W * 32 * R;
   const int64_t row_tiles = (n_rows + rows_per_block - 1) / rows_per_block;
   const int64_t resident = (int64_t)num_sms() * per_sm;
   const int64_t target = resident * 2;
@@ -326,10 +312,10 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   a.out = out;
   a.out_phi = out_phi;
   a.upper_only = kInter && uses_mirror(info);
-  a.shared_rows = shared_rows ? 1 : 0;
   a.n_splits = (int)splits;
   a.n_bgroups = nbg;
   a.tiles_per_batch = tiles_per_batch;
+  a.n_batches = n_batches;
   a.tile_w = shap_tile_w(info);
   a.M = info->n_features;
   a.G = info->n_groups;
@@ -341,7 +327,9 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
     if (xt != nullptr) cudaFreeAsync(xt, st);
     return fail(GTS_ERR_INVALID_ARGUMENT, "too many rows");
   }
-  kern<<<(unsigned)blocks, W * 32, smem, st>>>(a);
+  // persistent grid: the resident blocks walk the work items in order (nodal_kernel)
+  const int64_t grid = std::min<int64_t>(blocks, resident);
+  kern<<<(unsigned)grid, W * 32, smem, st>>>(a);
   gts_status s = cuda_check("nodal kernel launch");
   if (xt != nullptr) cudaFreeAsync(xt, st);  // stream-ordered: after the kernel
   if (s != GTS_OK || !a.upper_only) return s;

@@ -1148,18 +1148,14 @@ struct Args {
   void* out;
   void* out_phi;  // interaction kernel only: if set, the phi_i cells are also added to phi (fused call)
   int upper_only;  // interaction kernel only: write cells (i, j) with i < j only; mirror_kernel fills (j, i)
-  // interaction kernel only: the W warps of a block share one row tile (32 R
-  // rows) and split each chunk's runs by work; their tiles are folded at each
-  // flush.  Wide models: a block's phi_ij rows shrink W-fold, so the rows in
-  // flight of all resident blocks stay in L2 and the flush REDs hit it.
-  int shared_rows;
   int n_splits;
-  // Block decomposition: blockIdx = ((batch * n_bgroups + g) * tiles_per_batch + tile) * n_splits + split.
+  // Work items (taken by persistent blocks): item = ((batch * n_bgroups + g) * n_splits + split) * tiles_per_batch + tile.
   // n_bgroups = 1: a block walks the chunks of every group (its split of them);
   // n_bgroups = G: a block walks group g's chunks only, so the blocks resident
   // at one time share one group's phi rows and the rows of one batch (L2 reuse).
   int n_bgroups;
   int64_t tiles_per_batch;
+  int64_t n_batches;  // work items = n_batches * n_bgroups * n_splits * tiles_per_batch (persistent grid)
   int tile_w;  // SHAP: row stride of the X / phi tiles = widest slot map + 1 (odd)
   int M, G;
   int64_t n_chunks;
@@ -1330,77 +1326,63 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   T* const sT = reinterpret_cast<T*>(g_smem);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int split = (int)(blockIdx.x % a.n_splits);
-  const int64_t bt = blockIdx.x / a.n_splits;                // (batch, group, tile)
-  const int64_t tile = bt % a.tiles_per_batch, bg = bt / a.tiles_per_batch;
-  const int64_t batch = bg / a.n_bgroups;
-  const int bgroup = (int)(bg % a.n_bgroups);
-  const int64_t row_tile = batch * a.tiles_per_batch + tile;
-  const bool shared_rows = kInter && a.shared_rows != 0;  // block-uniform
-  const int64_t rows_per_block = shared_rows ? ROWS : W * ROWS;
-  const int64_t row0 = row_tile * rows_per_block + (shared_rows ? 0 : (int64_t)warp * ROWS);
-  if (row_tile * rows_per_block >= a.n_rows) return;  // padding tile of the last batch (uniform per block)
+  // Persistent blocks (grid = the resident blocks): block b takes work items
+  // b, b + gridDim.x, ...; item = ((batch * n_bgroups + g) * n_splits + split)
+  // * tiles_per_batch + tile, so the items running at one time are mostly
+  // different row tiles of the same (group, split) and walk the same chunk
+  // stream in step: each staged chunk is read from HBM about once per wave and
+  // from L2 by the other blocks.  (With one block per item, blocks started as
+  // others retired, drifted apart along the stream and re-read it from HBM:
+  // 721 GB per 65 536-row covtype launch, profiles/r02g.)
+  constexpr int64_t rows_per_block = W * ROWS;
+  int64_t row0 = 0, c_begin = 0, c_end = 0;
+  int split = 0, bgroup = 0;
 
-  // this block's chunk range: all chunks, or group bgroup's (chunks are in group order)
-  int64_t g_lo = 0, g_hi = a.n_chunks;
-  if (a.n_bgroups > 1) {
-    auto first_of = [&](int g) -> int64_t {  // first chunk with group >= g
-      int64_t lo = 0, hi = a.n_chunks;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (chunks[mid].group < g) lo = mid + 1; else hi = mid;
-      }
-      return lo;
-    };
-    g_lo = first_of(bgroup);
-    g_hi = first_of(bgroup + 1);
-  }
-  const double w_lo = work[g_lo], w_span = work[g_hi] - w_lo;
-  auto split_begin = [&](int s) -> int64_t {
-    if (s >= a.n_splits) return g_hi;
-    const double target = w_lo + w_span * (double)s / (double)a.n_splits;
-    int64_t lo = g_lo, hi = g_hi;  // first c with work[c] >= target
+  auto first_of = [&](int g) -> int64_t {  // first chunk with group >= g (chunks are in group order)
+    int64_t lo = 0, hi = a.n_chunks;
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
-      if (work[mid] < target) lo = mid + 1; else hi = mid;
+      if (chunks[mid].group < g) lo = mid + 1; else hi = mid;
     }
     return lo;
   };
-  const int64_t c_begin = split_begin(split), c_end = split_begin(split + 1);
+  // the item's chunk range: its split of all chunks, or of group bgroup's
+  auto chunk_range = [&]() {
+    int64_t g_lo = 0, g_hi = a.n_chunks;
+    if (a.n_bgroups > 1) {
+      g_lo = first_of(bgroup);
+      g_hi = first_of(bgroup + 1);
+    }
+    const double w_lo = work[g_lo], w_span = work[g_hi] - w_lo;
+    auto split_begin = [&](int sp) -> int64_t {
+      if (sp >= a.n_splits) return g_hi;
+      const double target = w_lo + w_span * (double)sp / (double)a.n_splits;
+      int64_t lo = g_lo, hi = g_hi;  // first c with work[c] >= target
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (work[mid] < target) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    c_begin = split_begin(split);
+    c_end = split_begin(split + 1);
+  };
 
-  // prologue: barriers, first chunk in flight, gauss table, zeroed tiles
+  // prologue (once per block): barriers, gauss table, TMEM
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_fence_init();
-    if (c_begin < c_end) {
-      const ChunkRec c0 = chunks[c_begin];
-      mbar_expect_tx(&bars[0], (uint32_t)c0.data_bytes);
-      tma_bulk_g2s(stage0, a.blob + c0.data_off, (uint32_t)c0.data_bytes, &bars[0]);
-    }
   }
   const T* gsrc = reinterpret_cast<const T*>(a.blob + hdr->off_gauss);
   for (int i = tid; i < kQMax * 3 * kQMax; i += blockDim.x) sT[i] = gsrc[i];
   int xb[R], ab[R];
-  int64_t row[R];
-  bool ok[R];
   constexpr int kXg = XG;
   static_assert((XG != 0) == xg_enabled<kInter, S>(), "X source");
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int lr = warp * ROWS + r * 32 + lane;
-    const int64_t rr = row0 + r * 32 + lane;
-    // kXg = 1: the row (the feature-major copy is padded to whole tiles); 2: the row's TMEM column base
-    xb[r] = kXg == 2 ? r * 64 : kXg ? (int)rr : o_x + lr * XS;
-    ab[r] = o_acc + lr * AS;
-    row[r] = row0 + r * 32 + lane;
-    ok[r] = row[r] < a.n_rows;
-    for (int i = 0; i < AW; ++i) sT[ab[r] + i] = (T)0;
-  }
   __shared__ uint32_t tm_base;
   uint32_t tm_warp = 0;
   if constexpr (kXg == 2) {
-    // 128 TMEM columns: this block's X rows, column r * 64 + f of lane (warp, lane)
+    // 128 TMEM columns: the current row tile's X, column r * 64 + f of lane (warp, lane)
     if (warp == 0) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tm_base)));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -1409,11 +1391,6 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     tm_warp = tm_base + ((uint32_t)(32 * (warp & 3)) << 16);
-    for (int f = 0; f < a.M; ++f) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) tm_st(tm_warp + r * 64 + f, X[(size_t)f * a.col_stride + row0 + r * 32 + lane]);
-    }
-    tm_wait_st();
   }
   const int M1 = a.M + 1;
   int cur_map = -1, cur_group = -1, cur_slots = 0;
@@ -1425,67 +1402,7 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   // row (coalesced RED) and the loads of the tile are independent (ILP).  One
   // atomic per non-zero (row, group, feature) cell.
   const int tile_row0 = warp * ROWS;
-  // Shared-rows flush (interactions): fold the W warps' tiles into warp 0's,
-  // then warp w flushes the slot rows i = w mod W of it, lane = row; the Eq. 6
-  // diagonal of slot i reads its whole row sum (cells (i, j > i) and (j < i, i)).
-  auto flush_shared = [&]() {
-    if constexpr (kInter) {
-      __syncthreads();
-      const int cells = ROWS * AS;
-      T* const t0 = sT + o_acc;
-      for (int i = tid; i < cells; i += W * 32) {
-        T v = t0[i];
-#pragma unroll
-        for (int w = 1; w < W; ++w) {
-          v += t0[w * cells + i];
-          t0[w * cells + i] = (T)0;
-        }
-        t0[i] = v;
-      }
-      __syncthreads();
-      int fm[S];
-#pragma unroll
-      for (int j = 0; j < S; ++j) fm[j] = j < cur_slots ? __ldg(slotmap + cur_map_begin + j) : 0;
-#pragma unroll 1
-      for (int r = 0; r < R; ++r) {
-        const int64_t rg = row0 + r * 32 + lane;
-        const bool ok_r = rg < a.n_rows;
-        const T* const tl = t0 + (r * 32 + lane) * AS;
-        T* const base = out + ((size_t)(ok_r ? rg : 0) * a.G + cur_group) * (size_t)M1 * M1;
-#pragma unroll
-        for (int i = 0; i < S; ++i) {
-          if (i < cur_slots && (i % W) == warp) {
-            T rs = (T)0;
-#pragma unroll
-            for (int j = 0; j < S; ++j) {
-              if (j != i && j < cur_slots) {
-                const int c = j > i ? i * (2 * S - i - 1) / 2 + j : j * (2 * S - j - 1) / 2 + i;
-                const T v = tl[c];
-                rs += v;
-                if (j > i && ok_r && v != (T)0) {
-                  atomicAdd(base + (size_t)fm[i] * M1 + fm[j], v);
-                  if (!a.upper_only) atomicAdd(base + (size_t)fm[j] * M1 + fm[i], v);
-                }
-              }
-            }
-            const T di = tl[i * (2 * S - i - 1) / 2 + i];  // Eq. 6: phi_ii = phi_i - sum_{j != i} phi_ij
-            const T d = di - rs;
-            if (ok_r && d != (T)0) atomicAdd(base + (size_t)fm[i] * (M1 + 1), d);
-            if (ok_r && a.out_phi != nullptr && di != (T)0)
-              atomicAdd(static_cast<T*>(a.out_phi) + ((size_t)rg * a.G + cur_group) * M1 + fm[i], di);
-          }
-        }
-      }
-      __syncthreads();
-      for (int i = tid; i < cells; i += W * 32) t0[i] = (T)0;
-    }
-  };
   auto flush = [&]() {
-    if (shared_rows) {
-      if (dirty) flush_shared();
-      dirty = false;
-      return;
-    }
     if (dirty) {
       __syncwarp();
       if constexpr (kInter) {
@@ -1590,49 +1507,78 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   };
 
   uint32_t phase[2] = {0u, 0u};
-  for (int64_t ci = c_begin; ci < c_end; ++ci) {
-    const int b = (int)((ci - c_begin) & 1);
-    const ChunkRec c = chunks[ci];
-    __syncthreads();  // every warp is done with buffer b^1 (chunk ci-1)
-    if (tid == 0 && ci + 1 < c_end) {  // prefetch the next chunk while this one computes
-      const ChunkRec cn = chunks[ci + 1];
-      mbar_expect_tx(&bars[b ^ 1], (uint32_t)cn.data_bytes);
-      tma_bulk_g2s(stage0 + (b ^ 1) * buf_bytes, a.blob + cn.data_off, (uint32_t)cn.data_bytes, &bars[b ^ 1]);
+  const int64_t n_items = (int64_t)a.n_batches * a.n_bgroups * a.n_splits * a.tiles_per_batch;
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int64_t tile = item % a.tiles_per_batch, bs = item / a.tiles_per_batch;  // (batch, group, split)
+    split = (int)(bs % a.n_splits);
+    const int64_t bg = bs / a.n_splits;
+    const int64_t batch = bg / a.n_bgroups;
+    bgroup = (int)(bg % a.n_bgroups);
+    const int64_t row_tile = batch * a.tiles_per_batch + tile;
+    if (row_tile * rows_per_block >= a.n_rows) continue;  // padding tile of the last batch (block-uniform)
+    row0 = row_tile * rows_per_block + (int64_t)warp * ROWS;
+    chunk_range();
+    __syncthreads();  // the previous item is done with both staging buffers and the tiles
+    if (tid == 0 && c_begin < c_end) {
+      const ChunkRec c0 = chunks[c_begin];
+      mbar_expect_tx(&bars[0], (uint32_t)c0.data_bytes);
+      tma_bulk_g2s(stage0, a.blob + c0.data_off, (uint32_t)c0.data_bytes, &bars[0]);
     }
-    if (c.map_id != cur_map || c.group != cur_group) {
-      flush();
-      if (!kXg && c.map_id != cur_map) gather(c);
-      cur_map = c.map_id;
-      cur_group = c.group;
-      cur_slots = c.n_slots;
-      cur_map_begin = c.slotmap_begin;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int lr = warp * ROWS + r * 32 + lane;
+      const int64_t rr = row0 + r * 32 + lane;
+      // kXg = 1: the row (the feature-major copy is padded to whole tiles); 2: the row's TMEM column base
+      xb[r] = kXg == 2 ? r * 64 : kXg ? (int)rr : o_x + lr * XS;
+      ab[r] = o_acc + lr * AS;
+      for (int i = 0; i < AW; ++i) sT[ab[r] + i] = (T)0;
     }
-    mbar_wait(&bars[b], phase[b]);
-    phase[b] ^= 1u;
-    if (row0 < a.n_rows) {
-      const int4* sE = reinterpret_cast<const int4*>(stage0 + b * buf_bytes);
-      const int4* sP = sE + c.n_elems;
-      const T* tab = reinterpret_cast<const T*>(sP + c.n_paths);
-      // shared rows: warp w takes the runs whose work midpoint falls in its W-th of the chunk's work
-      const double cw = shared_rows ? work[ci + 1] - work[ci] : 0.0;
-      double cum = 0.0;
-      for (int p = 0; p < c.n_paths;) {
-        const int4 ph = sP[p];
-        bool mine = true;
-        if (shared_rows) {
-          const double wr = (ph.x >> 16) * nodal_inter_flops(ph.x & 0xff, ph.y);
-          mine = min(W - 1, (int)((double)W * (cum + 0.5 * wr) / cw)) == warp;
-          cum += wr;
-        }
-        if (mine)
+    if constexpr (kXg == 2) {
+      for (int f = 0; f < a.M; ++f) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) tm_st(tm_warp + r * 64 + f, X[(size_t)f * a.col_stride + row0 + r * 32 + lane]);
+      }
+      tm_wait_st();
+    }
+    cur_map = -1;
+    cur_group = -1;
+    cur_slots = 0;
+    cur_map_begin = 0;
+    dirty = false;
+    for (int64_t ci = c_begin; ci < c_end; ++ci) {
+      const int b = (int)((ci - c_begin) & 1);
+      const ChunkRec c = chunks[ci];
+      __syncthreads();  // every warp is done with buffer b^1 (chunk ci-1)
+      if (tid == 0 && ci + 1 < c_end) {  // prefetch the next chunk while this one computes
+        const ChunkRec cn = chunks[ci + 1];
+        mbar_expect_tx(&bars[b ^ 1], (uint32_t)cn.data_bytes);
+        tma_bulk_g2s(stage0 + (b ^ 1) * buf_bytes, a.blob + cn.data_off, (uint32_t)cn.data_bytes, &bars[b ^ 1]);
+      }
+      if (c.map_id != cur_map || c.group != cur_group) {
+        flush();
+        if (!kXg && c.map_id != cur_map) gather(c);
+        cur_map = c.map_id;
+        cur_group = c.group;
+        cur_slots = c.n_slots;
+        cur_map_begin = c.slotmap_begin;
+      }
+      mbar_wait(&bars[b], phase[b]);
+      phase[b] ^= 1u;
+      if (row0 < a.n_rows) {
+        const int4* sE = reinterpret_cast<const int4*>(stage0 + b * buf_bytes);
+        const int4* sP = sE + c.n_elems;
+        const T* tab = reinterpret_cast<const T*>(sP + c.n_paths);
+        for (int p = 0; p < c.n_paths;) {
+          const int4 ph = sP[p];
           run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S), kXg, (S / 2 < kQMax ? S / 2 : kQMax)>(
               ph, sE, tab, sT, xb, ab, X, kXg == 2 ? (int)tm_warp : (int)a.col_stride);
-        p += ph.x >> 16;
+          p += ph.x >> 16;
+        }
+        dirty = true;
       }
-      dirty = true;
     }
+    flush();
   }
-  flush();
   if constexpr (kXg == 2) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();

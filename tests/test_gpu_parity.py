@@ -504,41 +504,3 @@ def test_validate_nonfinite_x(gpu, dtype):
         ex.shap_device(y)
     ex.shap_device(x)
 
-
-# ------------------------- shared-row interaction blocks (wide-model phi_ij in L2)
-
-SHARED = [
-    # (workload, trees kept, rows, fused): ragged row counts, several 32-row tiles
-    ("cal_housing-med", 100, 77, False),
-    ("adult-large", 120, 45, True),
-    ("covtype-large", 80, 40, True),
-    ("fashion_mnist-med", 60, 37, True),
-]
-
-
-@pytest.mark.parametrize("dtype", DTYPES)
-@pytest.mark.parametrize("case", SHARED, ids=[c[0] for c in SHARED])
-def test_shared_row_interaction_blocks(gpu, case, dtype, monkeypatch):
-    """The interaction kernel with the W warps of a block on one row tile
-    (runs split by work, tiles folded at each flush; forced on for every model
-    with GTS_INTER_SHARED_ROWS=2, automatic for fashion_mnist) against O6, the
-    fused call's SHAP values against O5, and equal to the per-warp-rows kernel."""
-    import torch
-    name, trees, n, fused = case
-    w = WORKLOADS[name]
-    ens = w.ensemble().subset(range(trees))
-    x = w.x(n, ens=ens)
-    ex = _explainer(ens, dtype, "nodal")
-    xd = torch.from_numpy(np.ascontiguousarray(x, dtype=ex.np_dtype)).cuda()
-    ref = oracle.interactions(ens, x.astype(np.float64))
-    monkeypatch.setenv("GTS_INTER_SHARED_ROWS", "2")
-    if fused:
-        phi, pij = ex.shap_and_interactions_device(xd)
-        parity.check(phi.cpu().numpy(), oracle.treeshap(ens, x.astype(np.float64)), dtype, f"{name} shared fused shap")
-    else:
-        pij = ex.interactions_device(xd)
-    got = pij.cpu().numpy()
-    parity.check(got, ref, dtype, f"{name} shared-row interactions")
-    monkeypatch.setenv("GTS_INTER_SHARED_ROWS", "0")
-    per_warp = ex.interactions_device(xd).cpu().numpy()
-    parity.check(got, per_warp.astype(np.float64), dtype, f"{name} shared vs per-warp rows")
