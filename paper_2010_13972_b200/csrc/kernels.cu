@@ -216,8 +216,11 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   constexpr int XG = nodal::xg_enabled<kInter, S>() ? 1 : 0;
   auto kern = nodal::nodal_kernel<T, S, W, R, kInter, XG>;
   if constexpr (XG == 1 && GTS_TMEM_X && sizeof(T) == 4 && S == 64 && W == 4 && R * 64 <= 128) {
-    // identity slot map (features = slots < 64): x from TMEM (nodal::load_x)
+    // identity slot map (features = slots < 64): x from TMEM by feature (nodal::load_x)
     if (info->n_features <= 64) kern = nodal::nodal_kernel<T, S, W, R, kInter, 2>;
+  }
+  if constexpr (XG == 1 && (GTS_TMEM_X & 2) && sizeof(T) == 4 && S == 32 && W == 4 && R * S <= 64) {
+    kern = nodal::nodal_kernel<T, S, W, R, kInter, 3>;  // per-chunk maps: x from TMEM by slot
   }
   const size_t smem = nodal_smem_bytes<T, kInter, S>(info);
   if (smem > 227 * 1024) return fail(GTS_ERR_INVALID_ARGUMENT, "chunk staging needs %zu bytes of shared memory", smem);

@@ -252,10 +252,18 @@ __device__ __forceinline__ void tm_st(uint32_t taddr, float v) {
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// TMEM column of an element's x within its row's block: the feature (kXg = 2,
+// identity maps) or the slot (kXg = 3, per-chunk maps; NT = 2 records hold the
+// slot's byte offset).
+template <typename T, int kXg>
+__device__ __forceinline__ int tm_col(int4 rec) {
+  return kXg == 2 ? rec.w : rec.z / (int)sizeof(T);
+}
+
 template <typename T, int NT, int kXg>
 __device__ __forceinline__ T load_x(const T* sT, int xb, int4 rec, const T* __restrict__ xg, int cs) {
-  if constexpr (kXg == 2) {
-    T v = (T)tm_ld((uint32_t)cs + (uint32_t)(xb + rec.w));
+  if constexpr (kXg >= 2) {
+    T v = (T)tm_ld((uint32_t)cs + (uint32_t)(xb + tm_col<T, kXg>(rec)));
     tm_wait_ld();
     tm_pin(v);
     return v;
@@ -299,12 +307,12 @@ __device__ __forceinline__ void shap_run(int k, int n_run, const int4* __restric
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = (T)0;
-      if constexpr (kXg == 2) xv[r][s] = (T)tm_ld((uint32_t)cs + (uint32_t)(xb[r] + e.w));
+      if constexpr (kXg >= 2) xv[r][s] = (T)tm_ld((uint32_t)cs + (uint32_t)(xb[r] + tm_col<T, kXg>(e)));
       else if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(e.w * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
       else xv[r][s] = sT[xb[r] + (NT == 2 ? e.z / (int)sizeof(T) : e.z)];
     }
   }
-  if constexpr (kXg == 2) {
+  if constexpr (kXg >= 2) {
     tm_wait_ld();
 #pragma unroll
     for (int s = 0; s < KM; ++s)
@@ -420,12 +428,12 @@ __device__ __forceinline__ void shap_run_x2(int k, int n_run, const int4* __rest
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       acc[r][s] = make_float2(0.f, 0.f);
-      if constexpr (kXg == 2) xv[r][s] = tm_ld((uint32_t)cs + (uint32_t)(xb[r] + e.w));
+      if constexpr (kXg >= 2) xv[r][s] = tm_ld((uint32_t)cs + (uint32_t)(xb[r] + tm_col<float, kXg>(e)));
       else if constexpr (kXg) xv[r][s] = __ldg(xg + (uint32_t)(e.w * cs + xb[0]) + r * 32);  // a lane's rows: 32 apart
       else xv[r][s] = sT[xb[r] + (NT == 2 ? e.z / (int)sizeof(float) : e.z)];
     }
   }
-  if constexpr (kXg == 2) {
+  if constexpr (kXg >= 2) {
     tm_wait_ld();
 #pragma unroll
     for (int s = 0; s < KM; ++s)
@@ -1178,7 +1186,8 @@ __host__ __device__ constexpr int tile_words_per_warp() {
 #define GTS_XG_FIXED_STRIDE 0  // global-X SHAP kernels: phi tile row stride S + 1 (compile time) or the blob's widest map + 1
 #endif
 #ifndef GTS_TMEM_X
-#define GTS_TMEM_X 1  // fp32 SHAP kernels with identity maps of <= 64 features keep X in TMEM (XG = 2)
+#define GTS_TMEM_X 3  // bit 0: fp32 SHAP kernels with identity maps of <= 64 features keep X in TMEM (XG = 2);
+                      // bit 1: the 32-slot fp32 SHAP kernel keeps each slot map's X in TMEM (XG = 3)
 #endif
 #ifndef GTS_XG_MIN_S
 #define GTS_XG_MIN_S 32  // SHAP kernels with >= this many slots read X from feature-major global memory
@@ -1305,7 +1314,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // in global memory, 2: TMEM filled from that copy; see load_x).
 template <typename T, int S, int W, int R, bool kInter, int XG>
 __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal_kernel(Args a) {
-  static_assert(XG != 2 || (sizeof(T) == 4 && W == 4 && R * 64 <= 128 && !kInter), "TMEM X: 4 warps = 128 lanes");
+  static_assert(XG < 2 || (sizeof(T) == 4 && W == 4 && !kInter), "TMEM X: 4 warps = 128 lanes");
+  static_assert(XG != 2 || R * 64 <= 128, "TMEM X by feature: 128 columns");
+  static_assert(XG != 3 || R * S <= 64, "TMEM X by slot: 64 columns");
+  constexpr int kTmCols = XG == 2 ? 128 : 64;
   const int XS = x_stride<kInter, S>(a.tile_w);
   const int AS = acc_stride<kInter, S>(a.tile_w);
   const int AW = kInter ? acc_width<kInter>(S) : a.tile_w - 1;  // cells per row
@@ -1381,10 +1393,12 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   static_assert((XG != 0) == xg_enabled<kInter, S>(), "X source");
   __shared__ uint32_t tm_base;
   uint32_t tm_warp = 0;
-  if constexpr (kXg == 2) {
-    // 128 TMEM columns: the current row tile's X, column r * 64 + f of lane (warp, lane)
+  if constexpr (kXg >= 2) {
+    // TMEM columns for the row tile's X: kXg = 2: column r * 64 + f of lane (warp, lane),
+    // filled once per item; kXg = 3: column r * S + slot, filled at each slot-map change
     if (warp == 0) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tm_base)));
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tm_base)),
+                   "n"(kTmCols));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1528,8 +1542,8 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
     for (int r = 0; r < R; ++r) {
       const int lr = warp * ROWS + r * 32 + lane;
       const int64_t rr = row0 + r * 32 + lane;
-      // kXg = 1: the row (the feature-major copy is padded to whole tiles); 2: the row's TMEM column base
-      xb[r] = kXg == 2 ? r * 64 : kXg ? (int)rr : o_x + lr * XS;
+      // kXg = 1: the row (the feature-major copy is padded to whole tiles); 2, 3: the row's TMEM column base
+      xb[r] = kXg == 2 ? r * 64 : kXg == 3 ? r * S : kXg ? (int)rr : o_x + lr * XS;
       ab[r] = o_acc + lr * AS;
       for (int i = 0; i < AW; ++i) sT[ab[r] + i] = (T)0;
     }
@@ -1557,6 +1571,15 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
       if (c.map_id != cur_map || c.group != cur_group) {
         flush();
         if (!kXg && c.map_id != cur_map) gather(c);
+        if (kXg == 3 && c.map_id != cur_map) {
+          // the new slot map's x values of this warp's rows into TMEM (lane = row)
+          for (int i = 0; i < c.n_slots; ++i) {
+            const size_t fo = (size_t)slotmap[c.slotmap_begin + i] * a.col_stride + row0 + lane;
+#pragma unroll
+            for (int r = 0; r < R; ++r) tm_st(tm_warp + r * S + i, X[fo + r * 32]);
+          }
+          tm_wait_st();
+        }
         cur_map = c.map_id;
         cur_group = c.group;
         cur_slots = c.n_slots;
@@ -1571,7 +1594,7 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
         for (int p = 0; p < c.n_paths;) {
           const int4 ph = sP[p];
           run_dispatch<T, R, kInter, kInter ? 3 : nodal_tables(S), kXg, (S / 2 < kQMax ? S / 2 : kQMax)>(
-              ph, sE, tab, sT, xb, ab, X, kXg == 2 ? (int)tm_warp : (int)a.col_stride);
+              ph, sE, tab, sT, xb, ab, X, kXg >= 2 ? (int)tm_warp : (int)a.col_stride);
           p += ph.x >> 16;
         }
         dirty = true;
@@ -1579,12 +1602,12 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
     }
     flush();
   }
-  if constexpr (kXg == 2) {
+  if constexpr (kXg >= 2) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm_base));
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base), "n"(kTmCols));
     }
   }
 }
