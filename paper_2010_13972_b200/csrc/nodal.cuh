@@ -1279,6 +1279,9 @@ __device__ __forceinline__ void mbar_fence_init() {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+#ifndef GTS_STAGGER
+#define GTS_STAGGER 4  // chunks of start rotation per row tile (persistent blocks, see nodal_kernel)
+#endif
 #ifndef GTS_TMA_POLICY
 #define GTS_TMA_POLICY 0  // L2 policy of the chunk copies: 0 default, 1 evict_normal, 2 evict_last, 3 evict_first
 #endif
@@ -1532,9 +1535,19 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
     if (row_tile * rows_per_block >= a.n_rows) continue;  // padding tile of the last batch (block-uniform)
     row0 = row_tile * rows_per_block + (int64_t)warp * ROWS;
     chunk_range();
+    // Staggered start: the item walks its chunks from a rotation of GTS_STAGGER
+    // chunks per row tile, so the blocks in flight cover a window of ~GTS_STAGGER
+    // x grid chunks of the stream (in L2) instead of requesting the same chunk
+    // at once (all blocks on one L2 line set).
+    const int64_t c_len = c_end - c_begin;
+    const int64_t rot = c_len > 0 ? (tile * GTS_STAGGER) % c_len : 0;
+    auto chunk_at = [&](int64_t j) -> int64_t {
+      const int64_t q = rot + j;
+      return c_begin + (q >= c_len ? q - c_len : q);
+    };
     __syncthreads();  // the previous item is done with both staging buffers and the tiles
-    if (tid == 0 && c_begin < c_end) {
-      const ChunkRec c0 = chunks[c_begin];
+    if (tid == 0 && c_len > 0) {
+      const ChunkRec c0 = chunks[chunk_at(0)];
       mbar_expect_tx(&bars[0], (uint32_t)c0.data_bytes);
       tma_bulk_g2s(stage0, a.blob + c0.data_off, (uint32_t)c0.data_bytes, &bars[0]);
     }
@@ -1559,12 +1572,12 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
     cur_slots = 0;
     cur_map_begin = 0;
     dirty = false;
-    for (int64_t ci = c_begin; ci < c_end; ++ci) {
-      const int b = (int)((ci - c_begin) & 1);
-      const ChunkRec c = chunks[ci];
-      __syncthreads();  // every warp is done with buffer b^1 (chunk ci-1)
-      if (tid == 0 && ci + 1 < c_end) {  // prefetch the next chunk while this one computes
-        const ChunkRec cn = chunks[ci + 1];
+    for (int64_t j = 0; j < c_len; ++j) {
+      const int b = (int)(j & 1);
+      const ChunkRec c = chunks[chunk_at(j)];
+      __syncthreads();  // every warp is done with buffer b^1 (the previous chunk)
+      if (tid == 0 && j + 1 < c_len) {  // prefetch the next chunk while this one computes
+        const ChunkRec cn = chunks[chunk_at(j + 1)];
         mbar_expect_tx(&bars[b ^ 1], (uint32_t)cn.data_bytes);
         tma_bulk_g2s(stage0 + (b ^ 1) * buf_bytes, a.blob + cn.data_off, (uint32_t)cn.data_bytes, &bars[b ^ 1]);
       }
