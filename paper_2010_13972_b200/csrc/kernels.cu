@@ -269,9 +269,19 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
     }
   }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // The occupancy query assumes the kernel's preferred shared-memory carveout;
+  // without one it reported 1 block per SM for kernels that run 3 (ncu:
+  // occupancy limits 3 / 3, profiles/r02j), which sized the persistent grid at
+  // one block per SM.  Ask for the largest carveout first.
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem) != cudaSuccess) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
   per_sm = std::max(per_sm, 1);
+  if (const char* e = getenv("GTS_DEBUG_LAUNCH"))
+    if (e[0] == '1') fprintf(stderr, "gts: nodal launch S=%d W=%d R=%d inter=%d smem=%zu per_sm=%d\n", S, W, R, (int)kInter, smem, per_sm);
   const int64_t rows_per_block = (int64_t)W * 32 * R;
   const int64_t row_tiles = (n_rows + rows_per_block - 1) / rows_per_block;
   const int64_t resident = (int64_t)num_sms() * per_sm;
@@ -295,14 +305,13 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
     splits = (target + tiles_per_batch - 1) / tiles_per_batch;
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, info->n_units / G));
   } else {
-    splits = (target + row_tiles - 1) / row_tiles;
-    // Blocks run in index order (row tile major, split minor), so the first
-    // `resident` blocks cover resident / splits row tiles.  Keep the rows in
-    // flight small enough that their X rows and one group's phi (phi_ij) rows
-    // stay in L2; splits only add one flush per split boundary.
+    // Persistent blocks take items tile-minor within a (batch, split), so the
+    // items in flight are up to tiles_per_batch row tiles of a few splits:
+    // batches keep those rows' X and phi (phi_ij) within the L2 budget.
     const int64_t bytes_per_row = (int64_t)sizeof(T) * (info->n_features + (kInter ? M1 * M1 : M1));
-    const int64_t want = (resident * rows_per_block * bytes_per_row + l2_budget - 1) / l2_budget;
-    splits = std::max(splits, std::min(want, row_tiles > 0 ? resident : 1));
+    tiles_per_batch = std::max<int64_t>(1, std::min<int64_t>(tiles_per_batch,
+                                                             l2_budget / (rows_per_block * bytes_per_row)));
+    splits = (target + tiles_per_batch - 1) / tiles_per_batch;
   }
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, std::min<int64_t>(info->n_units, 1024)));
   const int64_t n_batches = (row_tiles + tiles_per_batch - 1) / tiles_per_batch;
