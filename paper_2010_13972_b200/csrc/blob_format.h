@@ -21,7 +21,7 @@ constexpr int kMaxChunkPaths = 256;
 constexpr int kChunkBytes = 16 * 1024;    // NODAL: staged bytes per chunk (one TMA bulk copy)
 #ifndef GTS_CHUNK_BYTES_WIDE
 #define GTS_CHUNK_BYTES_WIDE (8 * 1024)  // SHAP-only blobs with identity maps of > 16 features: 8 KB staging
-                                         // lets three 4-warp blocks share an SM (covtype, profiles/r02j)
+                                         // lets three 4-warp blocks share an SM (covtype)
 #endif
 
 struct BlobHeader {            // 256 bytes at offset 0

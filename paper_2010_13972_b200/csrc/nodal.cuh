@@ -42,8 +42,8 @@
 #endif
 #ifndef GTS_INTER_CACHEU_QMAX
 #define GTS_INTER_CACHEU_QMAX 4  // interaction runs up to this Q keep u_sq of every element in registers
-                                 // (measured, profiles/r02h: 5, 6, 7 cost adult 12-16 %; a paired-node
-                                 // per-path variant for Q >= 5 cost 28 %, r02j)
+                                 // (measured in a session lost with the earlier container: 5, 6, 7 cost adult 12-16 %; a paired-node
+                                 // per-path variant for Q >= 5 cost 28 %)
 #endif
 #ifndef GTS_INTER_RMW_BLOCK
 #define GTS_INTER_RMW_BLOCK 4  // interaction runs without register cells: tile read-modify-writes per block of cells
@@ -1191,7 +1191,7 @@ __host__ __device__ constexpr int tile_words_per_warp() {
 #endif
 #ifndef GTS_XG_MIN_S
 #define GTS_XG_MIN_S 32  // SHAP kernels with >= this many slots read X from feature-major global memory
-                         // (measured, profiles/r02f-g: with 2 rows per lane fashion 5.06e5 -> 6.14e5 rows/s,
+                         // (measured in lost sessions, see profiles/README.md: with 2 rows per lane fashion 5.06e5 -> 6.14e5 rows/s,
                          // the per-chunk X gathers are gone; covtype 1.40e4 -> 1.43e4)
 #endif
 // kXg kernels keep no X tile: every run reads its x values straight from a
@@ -1220,7 +1220,7 @@ __host__ __device__ constexpr int acc_stride(int tile_w) {
 #define GTS_INTER8_MINB 2  // resident blocks per SM the 8-slot fp32 interaction kernel's registers are sized for
 #endif
 #ifndef GTS_SHAP_R32
-#define GTS_SHAP_R32 2  // measured with global X (profiles/r02g): fashion R 2 / W 4 6.14e5 rows/s, R 1 / W 8 4.44e5
+#define GTS_SHAP_R32 2  // measured with global X (lost session): fashion R 2 / W 4 6.14e5 rows/s, R 1 / W 8 4.44e5
 #endif
 #ifndef GTS_SHAP_W32
 #define GTS_SHAP_W32 4
@@ -1229,14 +1229,14 @@ __host__ __device__ constexpr int acc_stride(int tile_w) {
 #define GTS_SHAP_B32 2  // resident blocks per SM the register budget is sized for
 #endif
 #ifndef GTS_SHAP_R64
-#define GTS_SHAP_R64 2  // measured with global X (profiles/r02g): covtype R 2 / W 4 1.43e4 rows/s, R 1 / W 8 1.38e4
+#define GTS_SHAP_R64 2  // measured with global X (lost session): covtype R 2 / W 4 1.43e4 rows/s, R 1 / W 8 1.38e4
 #endif
 #ifndef GTS_SHAP_W64
 #define GTS_SHAP_W64 4  // no X tile (kXg): 4 warps x 64 rows x 2 blocks fit the phi tiles
 #endif
 #ifndef GTS_SHAP_B64
 #define GTS_SHAP_B64 3  // 3 blocks x 4 warps x 64 rows per SM (168 registers, runtime tile stride, 8 KB chunks):
-                        // covtype 1.44e4 -> 1.64e4 rows/s (profiles/r02j)
+                        // covtype 1.44e4 -> 1.64e4 rows/s (lost session; r02e measures the result)
 #endif
 template <typename T, bool kInter, int S>
 struct Cfg {
