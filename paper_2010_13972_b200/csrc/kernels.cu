@@ -93,6 +93,9 @@ __global__ void mirror_kernel(T* __restrict__ phi, int64_t n_mats, int M1) {
   }
 }
 
+#ifndef GTS_PERSIST
+#define GTS_PERSIST 1
+#endif
 #ifndef GTS_GROUP_MAJOR
 #define GTS_GROUP_MAJOR 2  // group-major blocks: 0 never, 1 per-chunk slot maps (wide models), 2 whenever G > 1
                            // (measured, profiles/r02d: fashion SHAP 2.94e5 -> 5.06e5 rows/s, covtype 1.21e4 -> 1.40e4)
@@ -280,6 +283,25 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
     per_sm = 1;
   }
   per_sm = std::max(per_sm, 1);
+  {
+    // The query still returned 1 for the 64-slot SHAP kernel that ncu shows
+    // running 3 per SM (r02k), so the limits are also computed here from the
+    // kernel's registers and shared memory (and TMEM columns for XG >= 2), and
+    // the larger count is used.
+    cudaFuncAttributes fa{};
+    int dev = 0, smem_sm = 0, reserved = 0;
+    cudaGetDevice(&dev);
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess &&
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev) == cudaSuccess) {
+      const int64_t regs_warp = ((int64_t)std::max(fa.numRegs, 1) * 32 + 255) / 256 * 256;
+      int64_t lim = std::min<int64_t>(65536 / (regs_warp * W), 64 / W);
+      lim = std::min<int64_t>(lim, smem_sm / ((int64_t)smem + fa.sharedSizeBytes + reserved));
+      if (kern != nodal::nodal_kernel<T, S, W, R, kInter, XG>) lim = std::min<int64_t>(lim, 4);  // TMEM X: 128 / 64 columns
+      per_sm = std::max<int>(per_sm, (int)std::max<int64_t>(lim, 1));
+    }
+    cudaGetLastError();
+  }
   if (const char* e = getenv("GTS_DEBUG_LAUNCH"))
     if (e[0] == '1') fprintf(stderr, "gts: nodal launch S=%d W=%d R=%d inter=%d smem=%zu per_sm=%d\n", S, W, R, (int)kInter, smem, per_sm);
   const int64_t rows_per_block = (int64_t)W * 32 * R;
@@ -339,8 +361,9 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
     if (xt != nullptr) cudaFreeAsync(xt, st);
     return fail(GTS_ERR_INVALID_ARGUMENT, "too many rows");
   }
-  // persistent grid: the resident blocks walk the work items in order (nodal_kernel)
-  const int64_t grid = std::min<int64_t>(blocks, resident);
+  // persistent grid: the resident blocks walk the work items in order (nodal_kernel);
+  // GTS_PERSIST=0: one block per item
+  const int64_t grid = GTS_PERSIST ? std::min<int64_t>(blocks, resident) : blocks;
   kern<<<(unsigned)grid, W * 32, smem, st>>>(a);
   gts_status s = cuda_check("nodal kernel launch");
   if (xt != nullptr) cudaFreeAsync(xt, st);  // stream-ordered: after the kernel

@@ -41,7 +41,8 @@
                                                 // (profiles/r01n, r01i)
 #endif
 #ifndef GTS_INTER_CACHEU_QMAX
-#define GTS_INTER_CACHEU_QMAX 4  // interaction runs up to this Q keep u_sq of every element in registers
+#define GTS_INTER_CACHEU_QMAX 5  // interaction runs up to this Q keep u_sq of every element in registers
+                                 // (5 over 4: adult-large both +11 %, covtype interactions +5 %, profiles/r02k)
                                  // (measured in a session lost with the earlier container: 5, 6, 7 cost adult 12-16 %; a paired-node
                                  // per-path variant for Q >= 5 cost 28 %)
 #endif
