@@ -1165,6 +1165,8 @@ struct Args {
   int n_bgroups;
   int64_t tiles_per_batch;
   int64_t n_batches;  // work items = n_batches * n_bgroups * n_splits * tiles_per_batch (persistent grid)
+  int tile_minor;     // 1: item = ((batch * n_bgroups + g) * n_splits + split) * tiles_per_batch + tile;
+                      // 0: item = ((batch * n_bgroups + g) * tiles_per_batch + tile) * n_splits + split
   int tile_w;  // SHAP: row stride of the X / phi tiles = widest slot map + 1 (odd)
   int M, G;
   int64_t n_chunks;
@@ -1527,9 +1529,18 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   uint32_t phase[2] = {0u, 0u};
   const int64_t n_items = (int64_t)a.n_batches * a.n_bgroups * a.n_splits * a.tiles_per_batch;
   for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int64_t tile = item % a.tiles_per_batch, bs = item / a.tiles_per_batch;  // (batch, group, split)
-    split = (int)(bs % a.n_splits);
-    const int64_t bg = bs / a.n_splits;
+    int64_t tile, bg;
+    if (a.tile_minor) {
+      tile = item % a.tiles_per_batch;
+      const int64_t bs = item / a.tiles_per_batch;  // (batch, group, split)
+      split = (int)(bs % a.n_splits);
+      bg = bs / a.n_splits;
+    } else {
+      split = (int)(item % a.n_splits);
+      const int64_t bt = item / a.n_splits;  // (batch, group, tile)
+      tile = bt % a.tiles_per_batch;
+      bg = bt / a.tiles_per_batch;
+    }
     const int64_t batch = bg / a.n_bgroups;
     bgroup = (int)(bg % a.n_bgroups);
     const int64_t row_tile = batch * a.tiles_per_batch + tile;
