@@ -1344,14 +1344,13 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   T* const sT = reinterpret_cast<T*>(g_smem);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // Persistent blocks (grid = the resident blocks): block b takes work items
-  // b, b + gridDim.x, ...; item = ((batch * n_bgroups + g) * n_splits + split)
-  // * tiles_per_batch + tile, so the items running at one time are mostly
-  // different row tiles of the same (group, split) and walk the same chunk
-  // stream in step: each staged chunk is read from HBM about once per wave and
-  // from L2 by the other blocks.  (With one block per item, blocks started as
-  // others retired, drifted apart along the stream and re-read it from HBM:
-  // 721 GB per 65 536-row covtype launch, profiles/r02g.)
+  // Block b takes work items b, b + gridDim.x, ... -- one item per block by
+  // default; with GTS_PERSIST=1 the grid is the resident blocks (kernels.cu).
+  // Items (Args::tile_minor): tile-minor within a (batch, group, split) for
+  // group-major models, so that the items in flight share a chunk stream;
+  // split-minor for single-group models, so that they share rows.  Items
+  // start their chunk walk at a rotation of GTS_STAGGER chunks per row tile.  (persistent blocks cut the chunk re-reads from HBM
+  // 721 -> 219 GB per 65 536-row covtype launch but measured slower.)
   constexpr int64_t rows_per_block = W * ROWS;
   int64_t row0 = 0, c_begin = 0, c_end = 0;
   int split = 0, bgroup = 0;
