@@ -93,10 +93,6 @@ __global__ void mirror_kernel(T* __restrict__ phi, int64_t n_mats, int M1) {
   }
 }
 
-#ifndef GTS_PERSIST
-#define GTS_PERSIST 0  // 1: persistent blocks (grid = resident blocks) walking the items tile-minor: 3.3x less DRAM
-                       // traffic on covtype SHAP but slower (covtype SHAP -3.5 %, fashion interactions -30 %, r02l)
-#endif
 #ifndef GTS_GROUP_MAJOR
 #define GTS_GROUP_MAJOR 2  // group-major blocks: 0 never, 1 per-chunk slot maps (wide models), 2 whenever G > 1
                            // (measured, profiles/r02d: fashion SHAP 2.94e5 -> 5.06e5 rows/s, covtype 1.21e4 -> 1.40e4)
