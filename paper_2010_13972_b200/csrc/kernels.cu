@@ -93,6 +93,10 @@ __global__ void mirror_kernel(T* __restrict__ phi, int64_t n_mats, int M1) {
   }
 }
 
+#ifndef GTS_TILE_MINOR
+#define GTS_TILE_MINOR 1  // item order: 0 split-minor, 1 tile-minor for group-major models, 2 always tile-minor,
+                          // 3 tile-minor for identity slot maps
+#endif
 #ifndef GTS_GROUP_MAJOR
 #define GTS_GROUP_MAJOR 2  // group-major blocks: 0 never, 1 per-chunk slot maps (wide models), 2 whenever G > 1
                            // (measured, profiles/r02d: fashion SHAP 2.94e5 -> 5.06e5 rows/s, covtype 1.21e4 -> 1.40e4)
@@ -316,6 +320,8 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   // that a batch's X and one group's outputs fit the L2 budget.
   const bool wide = info->max_slots < info->n_features;
   const int nbg = (G > 1 && (GTS_GROUP_MAJOR == 2 || (GTS_GROUP_MAJOR == 1 && wide))) ? G : 1;
+  const bool tile_minor = GTS_TILE_MINOR == 2 || GTS_PERSIST || (GTS_TILE_MINOR == 1 && nbg > 1) ||
+                          (GTS_TILE_MINOR == 3 && !wide);
   int64_t tiles_per_batch = std::max<int64_t>(row_tiles, 1), splits;
   if (nbg > 1) {
     const int64_t bytes_per_row = (int64_t)sizeof(T) * (info->n_features + (kInter ? M1 * M1 : M1));
@@ -323,7 +329,7 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
                                                              l2_budget / (rows_per_block * bytes_per_row)));
     splits = (target + tiles_per_batch - 1) / tiles_per_batch;
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, info->n_units / G));
-  } else if (GTS_PERSIST) {
+  } else if (tile_minor) {
     // Persistent blocks take items tile-minor within a (batch, split), so the
     // items in flight are up to tiles_per_batch row tiles of a few splits:
     // batches keep those rows' X and phi (phi_ij) within the L2 budget.
@@ -359,7 +365,7 @@ gts_status launch_nodal(const gts_blob_info* info, const char* d_blob, const voi
   // item order: tile-minor (the items in flight share a chunk stream) for
   // persistent blocks and group-major models, split-minor (they share rows)
   // for single-group models with one block per item (cal_housing both: +6 %, r02l)
-  a.tile_minor = (GTS_PERSIST || nbg > 1) ? 1 : 0;
+  a.tile_minor = tile_minor ? 1 : 0;
   a.tile_w = shap_tile_w(info);
   a.M = info->n_features;
   a.G = info->n_groups;
