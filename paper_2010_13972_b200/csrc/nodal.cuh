@@ -1350,10 +1350,11 @@ __global__ void __launch_bounds__(W * 32, (Cfg<T, kInter, S>::kMinBlocks)) nodal
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // Block b takes work items b, b + gridDim.x, ... -- one item per block by
   // default; with GTS_PERSIST=1 the grid is the resident blocks (kernels.cu).
-  // Items (Args::tile_minor): tile-minor within a (batch, group, split) for
-  // group-major models, so that the items in flight share a chunk stream;
-  // split-minor for single-group models, so that they share rows.  Items
-  // start their chunk walk at a rotation of GTS_STAGGER chunks per row tile.  (persistent blocks cut the chunk re-reads from HBM
+  // Items (Args::tile_minor): tile-minor within a (batch, group, split), so
+  // that the items in flight share a chunk stream, except for SHAP with
+  // per-chunk slot maps: split-minor, so that they share rows (kernels.cu,
+  // GTS_TILE_MINOR).  Items start their chunk walk at a rotation of
+  // GTS_STAGGER chunks per row tile.  (persistent blocks cut the chunk re-reads from HBM
   // 721 -> 219 GB per 65 536-row covtype launch but measured slower.)
   constexpr int64_t rows_per_block = W * ROWS;
   int64_t row0 = 0, c_begin = 0, c_end = 0;
